@@ -1,0 +1,210 @@
+/*
+ * seisgpu.h -- C ABI of libseisgpu.so, the B200 (sm_100a) hot path of
+ * Anderson-accelerated FWI / LSRTM (arXiv:2008.11778).
+ *
+ * The reference package (seisopt, pure Python) has no native layer; its
+ * "plugin API" for this path is the duck-typed objective protocol
+ * (seisopt/optim/problems.py:1-5) and the module functions below it.  Each
+ * entry point here replaces one reference routine, named in its comment as
+ * seisopt/<file>:<line>.  A ctypes shim (paper_2008_11778_b200/_lib.py) binds
+ * these symbols and re-exposes the reference's Python signatures.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "dev" pointers are CUDA device pointers
+ *    on the handle's device; "host" pointers are ordinary host memory.
+ *  - Element type of every wavefield / gather / model buffer is the handle's
+ *    dtype (SG_F32 -> float, SG_F64 -> double) unless stated.
+ *  - Arrays are C-order.  Physical grid (nz, nx), x fastest
+ *    (seisopt/grid.py:5).  Gathers are (shots, nt, n_rec), time-major
+ *    (seisopt/wavesim.py:74).
+ *  - Every call returns 0 (SG_OK) or an SG_ERR_* code; sg_last_error() holds
+ *    the message (thread-local).  The shim maps codes to the reference's
+ *    exceptions: SG_ERR_ARG -> ValueError, SG_ERR_STABILITY ->
+ *    StabilityError (seisopt/wavesim.py:41), SG_ERR_EMPTY -> EmptyWindowError
+ *    (seisopt/optim/qr.py:18), SG_ERR_MODEL -> "model is not positive and
+ *    finite" (seisopt/gradients.py:312-331).
+ *  - Work is enqueued on the stream set by sg_set_stream (default: the
+ *    legacy default stream).  Calls that return host scalars synchronise.
+ */
+#ifndef SEISGPU_H
+#define SEISGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SG_OK 0
+#define SG_ERR_ARG 1
+#define SG_ERR_STABILITY 2
+#define SG_ERR_EMPTY 3
+#define SG_ERR_CUDA 4
+#define SG_ERR_OOM 5
+#define SG_ERR_MODEL 6
+#define SG_ERR_STATE 7
+
+#define SG_F32 4
+#define SG_F64 8
+
+/* forward-wavefield reconstruction for gradients / Born adjoints */
+#define SG_RECON_FULL 0       /* whole acceleration history in HBM */
+#define SG_RECON_CHECKPOINT 1 /* state checkpoints + segment recompute (bitwise) */
+#define SG_RECON_AUTO 2       /* FULL when it fits, else CHECKPOINT */
+
+typedef struct sg_desc {
+  int32_t nz, nx;                    /* physical grid, seisopt/grid.py:35-61 */
+  int32_t pad_top, pad_bottom;       /* PadSpec, seisopt/wavesim.py:108-123 */
+  int32_t pad_left, pad_right;
+  int32_t nt;                        /* time steps, seisopt/grid.py:123 */
+  int32_t n_shots;                   /* sources in the geometry */
+  int32_t n_rec;                     /* receivers */
+  int32_t dtype;                     /* SG_F32 | SG_F64 */
+  int32_t order;                     /* 2 (seisopt 5-point) | 8 (BASELINE configs) */
+  int32_t recon;                     /* SG_RECON_* */
+  int32_t batch;                     /* max shots per launch, 0 = auto (memory) */
+  int32_t checkpoint_every;          /* CHECKPOINT interval, 0 = auto (~sqrt(nt)) */
+  int32_t device;                    /* CUDA ordinal */
+  int32_t use_graphs;                /* capture time loops in CUDA graphs (1) */
+  int32_t reserved[4];
+  double dx, dz, dt;                 /* metres, seconds */
+  double cfl_safety;                 /* SimConfig.cfl_safety, seisopt/wavesim.py:57 */
+  double mem_budget_bytes;           /* 0 = 90% of free device memory */
+} sg_desc;
+
+typedef struct sg_handle sg_handle;
+typedef struct sg_aa sg_aa;
+
+const char* sg_last_error(void);
+int sg_version(void);
+
+/* ---- propagator context: replaces seisopt.wavesim.Workspace
+ *      (seisopt/wavesim.py:183-214), built once per geometry rather than per
+ *      call ------------------------------------------------------------------ */
+int sg_create(const sg_desc* desc, sg_handle** out);
+int sg_destroy(sg_handle* h);
+int sg_set_stream(sg_handle* h, void* cuda_stream);
+
+/* Sponge profiles pz (nzp) and px (nxp); damp = outer(pz, px)
+ * (seisopt/wavesim.py:150-165).  host f64. */
+int sg_set_sponge(sg_handle* h, const double* pz, const double* px);
+
+/* Bilinear taps from seisopt/wavesim.py:168-180, computed host-side by the
+ * shim (bit-identical restatement) and passed through unchanged:
+ * rows/cols (4, n) int32 padded-grid indices, weights (4, n) f64.  Source
+ * weights are pre-multiplied by nothing; src_scale = 1/(dx dz)
+ * (seisopt/wavesim.py:214).  host pointers. */
+int sg_set_geometry(sg_handle* h, const int32_t* src_rows, const int32_t* src_cols,
+                    const double* src_w, const int32_t* rec_rows,
+                    const int32_t* rec_cols, const double* rec_w, double src_scale);
+
+/* Source wavelet amplitudes (nt) f64 host, seisopt/grid.py:158-176. */
+int sg_set_wavelet(sg_handle* h, const double* amp);
+
+/* Squared slowness m (nz, nx), device pointer, element type m_dtype
+ * (SG_F32|SG_F64).  Validates positivity/finiteness (SG_ERR_MODEL,
+ * seisopt/gradients.py:312-316) and the CFL bound (SG_ERR_STABILITY,
+ * seisopt/wavesim.py:187-193; 8th order scaled by sqrt(4/6.5016)), then
+ * forms 1/m on the padded grid (seisopt/wavesim.py:200-201).  Synchronises. */
+int sg_set_model(sg_handle* h, const void* m_dev, int32_t m_dtype);
+
+/* ---- sweeps --------------------------------------------------------------- */
+
+/* Forward-model shots [shot0, shot0+count): gathers_dev (count, nt, n_rec).
+ * Replaces fwi_synthetic, seisopt/gradients.py:98-115 (each shot one
+ * _forward_sweep, seisopt/wavesim.py:259-304, keep_accel=False). */
+int sg_fwi_synthetic(sg_handle* h, int32_t shot0, int32_t count, void* gathers_dev);
+
+/* Forward + trapezoidal L2 misfit against observed (count, nt, n_rec) dev;
+ * *misfit_host = 1/2 dt sum_t w_t sum_r (f-g)^2 summed over the shots.
+ * Replaces FwiObjective.value -> fwi_synthetic + misfit_l2,
+ * seisopt/gradients.py:318-326, :70-79. */
+int sg_fwi_misfit(sg_handle* h, int32_t shot0, int32_t count, const void* observed_dev,
+                  double* misfit_host);
+
+/* Misfit and exact adjoint-state gradient over shots [shot0, shot0+count).
+ * grad_dev (nz, nx) receives fold_pad(sum_s image_s) of these shots
+ * (seisopt/gradients.py:118-155; fold seisopt/wavesim.py:135-147).  With
+ * accumulate != 0 the gradient is added to grad_dev.  Synchronises. */
+int sg_fwi_gradient(sg_handle* h, int32_t shot0, int32_t count, const void* observed_dev,
+                    double* misfit_host, void* grad_dev, int32_t accumulate);
+
+/* Born modelling about the current model as background
+ * (BornKernel, seisopt/gradients.py:158-220).
+ *  sg_born_forward : data_dev (count, nt, n_rec) = L m_r for m_r (nz, nx) dev
+ *                    (seisopt/gradients.py:191-205).
+ *  sg_born_adjoint : image_dev (nz, nx) = L^T data (seisopt/gradients.py:207-220).
+ *  sg_lsrtm_gradient: J = 1/2 ||L m_r - d_r||^2, grad = L^T (L m_r - d_r)
+ *                    (seisopt/gradients.py:253-277).
+ * The background acceleration history is cached in HBM when it fits
+ * (sg_born_cache), otherwise recomputed (lock-step forward, checkpointed
+ * adjoint). */
+int sg_born_cache(sg_handle* h, int32_t shot0, int32_t count, int32_t enable);
+int sg_born_forward(sg_handle* h, int32_t shot0, int32_t count, const void* m_r_dev,
+                    void* data_dev);
+int sg_born_adjoint(sg_handle* h, int32_t shot0, int32_t count, const void* data_dev,
+                    void* image_dev, int32_t accumulate);
+int sg_lsrtm_gradient(sg_handle* h, int32_t shot0, int32_t count, const void* m_r_dev,
+                      const void* d_r_dev, double* value_host, void* grad_dev,
+                      int32_t accumulate);
+
+/* Single-shot forward with the full acceleration history returned
+ * (forward_solve with keep_history, seisopt/wavesim.py:354-378):
+ * gather_dev (nt, n_rec), accel_dev (nt, nzp, nxp) padded grid. */
+int sg_forward_history(sg_handle* h, int32_t shot, void* gather_dev, void* accel_dev);
+
+/* Adjoint sweep of one data set returning v_n (adjoint_solve,
+ * seisopt/wavesim.py:414-430): ybar_dev (nt, n_rec), v_dev (nt, nzp, nxp). */
+int sg_adjoint_history(sg_handle* h, const void* ybar_dev, void* v_dev);
+
+/* Diagnostics: shots per batch chosen, reconstruction mode in use, bytes held. */
+int sg_query(sg_handle* h, int32_t* batch, int32_t* recon, double* device_bytes);
+
+/* Times `reps` launches of one step kernel (0 = forward+history store,
+ * 1 = adjoint+imaging, 2 = forward no history) over `count` shots with CUDA
+ * events on the handle's stream; *ms_per_launch = mean duration. */
+int sg_time_step_kernel(sg_handle* h, int32_t which, int32_t count, int32_t reps,
+                        float* ms_per_launch);
+
+/* Number of kernel launches this handle (or AA window) has issued. */
+int64_t sg_launch_count(void);
+
+/* ---- Anderson acceleration window on the device -------------------------
+ * Replaces AAWindow / SlidingQR / aa_weights / aa_step
+ * (seisopt/optim/anderson.py:55-148, seisopt/optim/qr.py:22-104) by a
+ * ring buffer of residual / G differences plus a fp64 Gram matrix updated
+ * with one fused pass per push; the m x m least-squares solve runs on the
+ * host in fp64 and reproduces the reference's window decisions
+ * (append-after-first-push, drop when ncols > memory, rank safeguard
+ * min|diag R| <= 1e-12 ||R||_F, zero basis for dependent columns). */
+int sg_aa_create(int64_t n, int32_t memory, int32_t dtype, int32_t device, sg_aa** out);
+int sg_aa_destroy(sg_aa* a);
+int sg_aa_set_stream(sg_aa* a, void* cuda_stream);
+int sg_aa_clear(sg_aa* a);                                   /* anderson.py:77-78 */
+int sg_aa_push(sg_aa* a, const void* p_dev, const void* g_dev); /* anderson.py:80-112 */
+int sg_aa_m_k(sg_aa* a);                                     /* anderson.py:69-71 */
+/* gamma (m_k), alpha (m_k+1), residual norm: anderson.py:115-123, :41-52 */
+int sg_aa_weights(sg_aa* a, double* gamma_host, double* alpha_host, double* resid_host,
+                  int32_t* m_k_host);
+/* p_out = G_k - sum gamma_i dG_i (beta == 1) or the alpha blend
+ * (anderson.py:126-148). gamma/alpha from sg_aa_weights (host). */
+int sg_aa_step(sg_aa* a, double beta, const double* gamma_host, const double* alpha_host,
+               void* p_out_dev);
+/* ||f_k||_2 (anderson.py:329) */
+int sg_aa_fk_norm(sg_aa* a, double* out_host);
+
+/* Device vector helpers for the optimizer loop (anderson.py:322, :362-370):
+ *  sg_vec_axpby : z = a x + b y            (x, y, z dev, length n)
+ *  sg_vec_dot2  : out[0] = <g, x>, out[1] = <g, y>   (fp64 accumulation)
+ *  sg_vec_stats : out = {min, max, max|x|, ||x||_2, nonfinite count} */
+int sg_vec_axpby(int64_t n, int32_t dtype, double a, const void* x, double b, const void* y,
+                 void* z, void* cuda_stream);
+int sg_vec_dot2(int64_t n, int32_t dtype, const void* g, const void* x, const void* y,
+                double* out_host, void* cuda_stream);
+int sg_vec_stats(int64_t n, int32_t dtype, const void* x, double* out_host,
+                 void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEISGPU_H */

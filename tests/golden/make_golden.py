@@ -1,0 +1,229 @@
+"""Generate golden vectors by running the UNMODIFIED reference package.
+
+Run in the build container (the reference is not on the GPU box):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+It imports ``seisopt`` from /root/reference/pkg/src and writes small ``.npz``
+fixtures next to this file.  The 8th-order fixtures use the one-method
+substitution documented in SURVEY.md s0 item 1: ``Workspace.laplacian`` is
+replaced by the 8th-order zero-exterior Laplacian and ``cfl_check`` is scaled
+by sqrt(4/6.5016); everything else (time loop, taps, sponge, imaging, fold,
+misfit, AA) is the reference's own code.  Library versions are recorded in
+each fixture.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+
+import numpy as np
+import scipy
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REF)
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from seisopt import gradients as G  # noqa: E402
+from seisopt import wavesim as W  # noqa: E402
+from seisopt.grid import (AcquisitionGeometry, Grid2D, ReflectivityModel,  # noqa: E402
+                          VelocityModel, make_ricker, smooth_model)
+from seisopt.optim import anderson as A  # noqa: E402
+
+from paper_2008_11778_b200 import synthetic  # noqa: E402  (input builders only)
+
+_ORIG_LAP = W.Workspace.laplacian
+_ORIG_CFL = W.cfl_check
+C8 = (-205.0 / 72.0, 8.0 / 5.0, -1.0 / 5.0, 8.0 / 315.0, -1.0 / 560.0)
+SYM8 = 205.0 / 72.0 + 2.0 * (8.0 / 5.0 + 1.0 / 5.0 + 8.0 / 315.0 + 1.0 / 560.0)
+
+
+def _lap8(self, u, out):
+    np.multiply(u, C8[0] * (self.rz + self.rx), out=out)
+    for k in range(1, 5):
+        c = C8[k] * self.rz
+        out[k:, :] += u[:-k, :] * c
+        out[:-k, :] += u[k:, :] * c
+    for k in range(1, 5):
+        c = C8[k] * self.rx
+        out[:, k:] += u[:, :-k] * c
+        out[:, :-k] += u[:, k:] * c
+    return out
+
+
+def _cfl8(model, dt=None, cfl_safety=1.0):
+    return _ORIG_CFL(model, dt, cfl_safety) * math.sqrt(4.0 / SYM8)
+
+
+def use_order(order):
+    if order == 8:
+        W.Workspace.laplacian = _lap8
+        W.cfl_check = _cfl8
+    else:
+        W.Workspace.laplacian = _ORIG_LAP
+        W.cfl_check = _ORIG_CFL
+
+
+def versions():
+    return dict(numpy=np.__version__, scipy=scipy.__version__)
+
+
+def ref_types(case):
+    """Rebuild a synthetic case with the reference's own types."""
+    g = case["grid"]
+    grid = Grid2D(nx=g.nx, nz=g.nz, dx=g.dx, dz=g.dz)
+    geo = case["geometry"]
+    geom = AcquisitionGeometry(geo.sources, geo.receivers, geo.dt, geo.nt)
+    w = case["wavelet"]
+    wav = make_ricker(w.peak_freq, geo.dt, geo.nt, t0=w.t0)
+    cfg = W.SimConfig(border_width=case["config"].border_width)
+    return grid, geom, wav, cfg
+
+
+class Recorder:
+    """Wraps an objective and records every model passed to value_and_grad."""
+
+    def __init__(self, inner):
+        self.inner = inner
+        self.counters = inner.counters
+        self.models = []
+
+    def value(self, p):
+        return self.inner.value(p)
+
+    def value_and_grad(self, p):
+        self.models.append(np.array(p, copy=True))
+        return self.inner.value_and_grad(p)
+
+
+def make_c1(order, with_aa):
+    use_order(order)
+    case = synthetic.c1_case(order=order)
+    grid, geom, wav, cfg = ref_types(case)
+    true = VelocityModel(grid, case["true"].m)
+    init = VelocityModel(grid, case["init"].m)
+    obs = G.fwi_synthetic(true, wav, geom, cfg)
+    ev = G.fwi_gradient(init, obs, wav, geom, cfg)
+    out = dict(m_true=true.m, m_init=init.m, obs_shot2=obs[2].samples,
+               value=ev.value, grad=ev.gradient, order=order, **versions())
+    if with_aa:
+        obj = Recorder(G.FwiObjective(grid, obs, wav, geom, cfg))
+        res = A.minimize_aa(obj, init.m.ravel(), memory=5, max_iters=20)
+        rows = np.array([[r.iteration, r.objective, r.grad_norm, r.grad_evals, r.obj_evals,
+                          r.step] for r in res.report.rows])
+        keep = [1, 2, 5, 10, 20]
+        out.update(aa_rows=rows, aa_eta=res.extras["eta"], aa_keep=np.array(keep),
+                   aa_iterates=np.stack([obj.models[k] for k in keep]),
+                   aa_final=res.p)
+    np.savez_compressed(os.path.join(HERE, f"c1_o{order}.npz"), **out)
+
+
+def small_setup(order, damp_top):
+    grid = Grid2D(nx=60, nz=40, dx=20.0, dz=20.0)
+    c = np.full(grid.shape, 1800.0)
+    c[15:, :] = 2200.0
+    c[28:, :] = 2600.0
+    model = smooth_model(VelocityModel.from_velocity(grid, c), 3.0)
+    sources = ((333.3, 0.0), (880.0, 47.5))
+    # receivers: fractional positions, an exact duplicate, and the far edge
+    # (x = extent_x clamps to j0 = nxp - 2 with tx = 1)
+    receivers = tuple((x, 30.0) for x in np.linspace(0.0, 1180.0, 25)) + (
+        (505.0, 37.5), (505.0, 37.5), (1180.0, 780.0))
+    geom = AcquisitionGeometry(sources, receivers, dt=2e-3, nt=300)
+    wav = make_ricker(12.0, 2e-3, 300, t0=0.08)
+    cfg = W.SimConfig(border_width=10, damp_top=damp_top)
+    return grid, model, geom, wav, cfg
+
+
+def make_small(order, damp_top):
+    use_order(order)
+    grid, model, geom, wav, cfg = small_setup(order, damp_top)
+    rng = np.random.default_rng(7)
+    c_true = model.velocity.copy()
+    c_true[18:24, 25:35] *= 1.06
+    true = VelocityModel.from_velocity(grid, c_true)
+    obs = G.fwi_synthetic(true, wav, geom, cfg)
+    syn = G.fwi_synthetic(model, wav, geom, cfg)
+    ev = G.fwi_gradient(model, obs, wav, geom, cfg)
+    kern = G.BornKernel(model, wav, geom, cfg)
+    m_r = rng.standard_normal(grid.shape) * 1e-8
+    born = kern.forward(m_r)
+    y = [W.ShotGather(s, rng.standard_normal((geom.nt, geom.n_receivers)), geom.dt)
+         for s in range(geom.n_sources)]
+    img = kern.adjoint(y)
+    lev = G.lsrtm_objective(model, m_r * 0.5, born, kernel=kern)
+    ws = W.Workspace(model, geom, cfg)
+    tag = f"small_o{order}_{'top' if damp_top else 'free'}"
+    np.savez_compressed(
+        os.path.join(HERE, tag + ".npz"),
+        m=model.m, m_true=true.m, obs=np.stack([o.samples for o in obs]),
+        syn=np.stack([s.samples for s in syn]), value=ev.value, grad=ev.gradient,
+        m_r=m_r, born=np.stack([b.samples for b in born]),
+        y=np.stack([v.samples for v in y]), img=img, lsrtm_value=lev.value,
+        lsrtm_grad=lev.gradient, rec_rows=ws.rec_rows, rec_cols=ws.rec_cols,
+        rec_w=ws.rec_w, src_rows=ws.src_rows, src_cols=ws.src_cols, src_w=ws.src_w,
+        damp=ws.damp, order=order, damp_top=damp_top, **versions())
+    # AA trajectory on the small FWI problem (drives the reference optimizer)
+    if order == 8 and damp_top:
+        obj = Recorder(G.FwiObjective(grid, obs, wav, geom, cfg))
+        res = A.minimize_aa(obj, model.m.ravel(), memory=3, max_iters=8)
+        rows = np.array([[r.iteration, r.objective, r.grad_norm, r.grad_evals, r.obj_evals,
+                          r.step] for r in res.report.rows])
+        obj_sd = G.FwiObjective(grid, obs, wav, geom, cfg)
+        sd = A.minimize_sd(obj_sd, model.m.ravel(), max_iters=3)
+        np.savez_compressed(os.path.join(HERE, "aa_fwi_small.npz"), rows=rows,
+                            eta=res.extras["eta"], iterates=np.stack(obj.models),
+                            final=res.p, lambdas=np.array(res.extras["lambdas"]),
+                            sd_final=sd.p, **versions())
+
+
+def make_aa_window():
+    """Window sequence with a full window, drops and a dependent column."""
+    use_order(2)
+    rng = np.random.default_rng(11)
+    n, memory = 500, 4
+    win = A.AAWindow(n, memory)
+    basis = rng.standard_normal((n, 3))
+    ps, gs, recs = [], [], []
+    for k in range(12):
+        p = rng.standard_normal(n) + basis @ rng.standard_normal(3)
+        g = rng.standard_normal(n) + basis @ rng.standard_normal(3)
+        if k == 7:  # make f_7 - f_6 parallel to f_6 - f_5 -> dependent column
+            f5 = gs[5] - ps[5]
+            f6 = gs[6] - ps[6]
+            g = p + f6 + 2.0 * (f6 - f5)
+        ps.append(p)
+        gs.append(g)
+        win.push(p, g)
+        rec = dict(m_k=win.m_k)
+        if win.m_k > 0:
+            w = A.aa_weights(win)
+            gamma = np.zeros(memory)
+            alpha = np.zeros(memory + 1)
+            gamma[: len(w.gamma)] = w.gamma
+            alpha[: len(w.alpha)] = w.alpha
+            rec.update(gamma=gamma, alpha=alpha, resid=w.residual_norm,
+                       step1=A.aa_step(win, 1.0, w), step_half=A.aa_step(win, 0.5, w))
+        else:
+            rec.update(gamma=np.zeros(memory), alpha=np.zeros(memory + 1), resid=np.nan,
+                       step1=A.aa_step(win), step_half=A.aa_step(win, 0.5))
+        recs.append(rec)
+    np.savez_compressed(
+        os.path.join(HERE, "aa_window.npz"), n=n, memory=memory, ps=np.stack(ps),
+        gs=np.stack(gs), m_k=np.array([r["m_k"] for r in recs]),
+        gamma=np.stack([r["gamma"] for r in recs]), alpha=np.stack([r["alpha"] for r in recs]),
+        resid=np.array([r["resid"] for r in recs]), step1=np.stack([r["step1"] for r in recs]),
+        step_half=np.stack([r["step_half"] for r in recs]), **versions())
+
+
+if __name__ == "__main__":
+    make_aa_window()
+    for order in (2, 8):
+        for top in (True, False):
+            make_small(order, top)
+    make_c1(2, with_aa=False)
+    make_c1(8, with_aa=True)
+    print("goldens written to", HERE)

@@ -1,0 +1,106 @@
+"""Pin the CPU oracle against golden vectors from the unmodified reference.
+
+The fixtures in tests/golden were produced by tests/golden/make_golden.py,
+which runs seisopt itself (2nd order) or seisopt with the one-method 8th-order
+Laplacian substitution.  The oracle must reproduce them to round-off; in
+practice it is bit-identical because it follows the reference's operation
+order.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from cases import c1, golden, oracle_setup, rel, small_case
+
+TOL = 1e-13
+
+
+@pytest.mark.parametrize("order", [2, 8])
+@pytest.mark.parametrize("damp_top", [True, False])
+def test_small_case(order, damp_top):
+    case = small_case(order, damp_top)
+    g = case["gold"]
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    st = oracle_setup(g["m"], grid, geom, cfg)
+    # bilinear taps and sponge: exact
+    for mine, name in zip(st.rec, ("rec_rows", "rec_cols", "rec_w")):
+        assert np.array_equal(mine, g[name])
+    for mine, name in zip(st.src, ("src_rows", "src_cols", "src_w")):
+        assert np.array_equal(mine, g[name])
+    assert np.array_equal(st.damp, g["damp"])
+    st_true = oracle_setup(g["m_true"], grid, geom, cfg)
+    obs = oracle.fwi_synthetic(st_true, wav.samples, geom.nt)
+    assert rel(np.stack(obs), g["obs"]) <= TOL
+    syn = oracle.fwi_synthetic(st, wav.samples, geom.nt)
+    assert rel(np.stack(syn), g["syn"]) <= TOL
+    val, grad, _ = oracle.fwi_gradient(st, list(g["obs"]), wav.samples, geom.nt)
+    assert abs(val - float(g["value"])) <= TOL * abs(float(g["value"]))
+    assert rel(grad, g["grad"]) <= TOL
+    born = oracle.BornOracle(st, wav.samples, geom.nt)
+    d = born.forward(g["m_r"])
+    assert rel(np.stack(d), g["born"]) <= TOL
+    img = born.adjoint(list(g["y"]))
+    assert rel(img, g["img"]) <= TOL
+    lval, lgrad = oracle.lsrtm_objective(born, g["m_r"] * 0.5, list(g["born"]))
+    assert abs(lval - float(g["lsrtm_value"])) <= TOL * abs(float(g["lsrtm_value"]))
+    assert rel(lgrad, g["lsrtm_grad"]) <= TOL
+
+
+@pytest.mark.parametrize("order", [2, 8])
+def test_c1_gradient(order):
+    case = c1(order)
+    g = case["gold"]
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    st_true = oracle_setup(g["m_true"], grid, geom, cfg)
+    obs = oracle.fwi_synthetic(st_true, wav.samples, geom.nt, threads=5)
+    assert rel(obs[2], g["obs_shot2"]) <= TOL
+    st = oracle_setup(g["m_init"], grid, geom, cfg)
+    val, grad, _ = oracle.fwi_gradient(st, obs, wav.samples, geom.nt, threads=5)
+    assert abs(val - float(g["value"])) <= TOL * float(g["value"])
+    assert rel(grad, g["grad"]) <= TOL
+
+
+def test_aa_window_sequence():
+    g = golden("aa_window")
+    n, memory = int(g["n"]), int(g["memory"])
+    win = oracle.AAWindowOracle(n, memory)
+    for k in range(len(g["ps"])):
+        win.push(g["ps"][k], g["gs"][k])
+        assert win.m_k == int(g["m_k"][k])
+        if win.m_k:
+            w = oracle.aa_weights(win)
+            assert np.allclose(w[0], g["gamma"][k][: win.m_k], rtol=1e-12, atol=1e-12)
+            assert np.array_equal(w[1], g["alpha"][k][: win.m_k + 1]) or np.allclose(
+                w[1], g["alpha"][k][: win.m_k + 1], rtol=1e-12, atol=1e-12)
+            assert abs(w[2] - g["resid"][k]) <= 1e-12 * max(1.0, abs(g["resid"][k]))
+            assert rel(oracle.aa_step(win, 1.0, w), g["step1"][k]) <= 1e-13
+            assert rel(oracle.aa_step(win, 0.5, w), g["step_half"][k]) <= 1e-13
+        else:
+            assert rel(oracle.aa_step(win), g["step1"][k]) == 0.0
+    # the dependent column pushed at k=7 must have shrunk the window
+    assert int(g["m_k"][7]) < min(7, memory)
+
+
+def test_aa_fwi_trajectory():
+    g = golden("aa_fwi_small")
+    case = small_case(8, True)
+    gs = case["gold"]
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+
+    def make(m):
+        return oracle_setup(m, grid, geom, cfg)
+
+    obj = oracle.FwiOracleObjective(make, list(gs["obs"]), wav.samples, geom.nt, grid.shape)
+    res = oracle.minimize_aa(obj, gs["m"].ravel(), memory=3, max_iters=8)
+    rows = np.array(res["rows"])
+    assert rows.shape == g["rows"].shape
+    assert np.array_equal(rows[:, [0, 3, 4]], g["rows"][:, [0, 3, 4]])
+    assert np.allclose(rows[:, 1], g["rows"][:, 1], rtol=1e-12)
+    assert np.array_equal(rows[:, 5], g["rows"][:, 5])
+    assert rel(res["p"], g["final"]) <= 1e-12
+    assert abs(res["eta"] - float(g["eta"])) <= 1e-15 * float(g["eta"])
+    # AA(0) == steepest descent
+    obj0 = oracle.FwiOracleObjective(make, list(gs["obs"]), wav.samples, geom.nt, grid.shape)
+    r0 = oracle.minimize_aa(obj0, gs["m"].ravel(), memory=0, max_iters=3)
+    assert rel(r0["p"], g["sd_final"]) == 0.0
