@@ -194,13 +194,18 @@ int sg_aa_step(sg_aa* a, double beta, const double* gamma_host, const double* al
 int sg_aa_fk_norm(sg_aa* a, double* out_host);
 
 /* Device vector helpers for the optimizer loop (anderson.py:322, :362-370):
- *  sg_vec_axpby : z = a x + b y            (x, y, z dev, length n)
- *  sg_vec_dot2  : out[0] = <g, x>, out[1] = <g, y>   (fp64 accumulation)
- *  sg_vec_stats : out = {min, max, max|x|, ||x||_2, nonfinite count} */
+ *  sg_vec_axpby      : z = a x + b y  (a == 1: z = x + b y, i.e. p - eta g)
+ *  sg_vec_lerp       : z = x + lam (y - x)            (blend candidate, :369)
+ *  sg_vec_blend_dots : out = {<g, pbar - p>, <g, ptil - pbar>}  (:363-364)
+ *  sg_vec_stats      : out = {min, max, max|x|, ||x||_2, nonfinite count}
+ * All device pointers of `dtype`, length n, fp64 accumulation. */
 int sg_vec_axpby(int64_t n, int32_t dtype, double a, const void* x, double b, const void* y,
                  void* z, void* cuda_stream);
-int sg_vec_dot2(int64_t n, int32_t dtype, const void* g, const void* x, const void* y,
-                double* out_host, void* cuda_stream);
+int sg_vec_lerp(int64_t n, int32_t dtype, const void* x, const void* y, double lam, void* z,
+                void* cuda_stream);
+int sg_vec_blend_dots(int64_t n, int32_t dtype, const void* g, const void* p,
+                      const void* pbar, const void* ptil, double* out_host,
+                      void* cuda_stream);
 int sg_vec_stats(int64_t n, int32_t dtype, const void* x, double* out_host,
                  void* cuda_stream);
 

@@ -1,0 +1,669 @@
+// sg_aa.cu -- Anderson-acceleration window (seisopt/optim/anderson.py:55-148,
+// seisopt/optim/qr.py:22-104) and the device vector helpers of the optimizer
+// loop (anderson.py:283-376).
+//
+// B200 design: the reference keeps an explicit thin QR (Q: N x m) and updates
+// it by CGS2 appends and Givens drops, ~6 m N words of traffic per iteration.
+// Here the window is a ring of m residual-difference columns DF and G
+// differences DG, plus an fp64 Gram matrix DF^T DF that one fused pass per
+// push extends (new row + projections of f_k), reading each stored column once
+// with fp64 accumulation.  The m x m problem (Cholesky, rank safeguard,
+// least-squares solve, alpha recovery) runs on the host in fp64 and reproduces
+// the reference's window decisions; the recombination is one more fused pass.
+// Per iteration: (m+4) reads + 4 writes (push) and (m+1) reads + 1 write
+// (step) of N-vectors.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "seisgpu.h"
+#include "sg_common.cuh"
+
+using namespace sg;
+
+namespace {
+
+constexpr int kMaxMem = 32;  // largest supported AA memory
+constexpr int kThreads = 256;
+constexpr int kBlocks = 148 * 4;
+
+struct Slots {
+  int s[kMaxMem];
+};
+struct Coefs {
+  double c[kMaxMem];
+};
+
+// fused push: f_k = g - p; df = f_k - f_prev; dg = g - g_prev; store df, dg
+// into slot `snew`; f_prev <- f_k, g_prev <- g; partial dots
+//   [0..nw)        <df, DF_i>
+//   nw             <df, df>
+//   [nw+1..2nw+1)  <f_k, DF_i>
+//   2nw+1          <f_k, df>
+//   2nw+2          <f_k, f_k>
+// first != 0: only f_prev/g_prev are written and <f_k, f_k> reduced.
+template <typename T, int MW>
+__global__ void __launch_bounds__(kThreads)
+    k_aa_push(const T* __restrict__ p, const T* __restrict__ g, T* __restrict__ fprev,
+              T* __restrict__ gprev, T* __restrict__ DF, T* __restrict__ DG, int64_t n,
+              const Slots slots, int nw, int snew, int first, double* __restrict__ part) {
+  double a_dd[MW], a_fd[MW];
+#pragma unroll
+  for (int i = 0; i < MW; ++i) a_dd[i] = a_fd[i] = 0.0;
+  double dd = 0.0, fd = 0.0, ff = 0.0;
+  T* dfn = DF + (int64_t)snew * n;
+  T* dgn = DG + (int64_t)snew * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const T gv = g[e];
+    const T fk = gv - p[e];  // seisopt/optim/anderson.py:84
+    const double fkd = (double)fk;
+    ff += fkd * fkd;
+    if (first) {
+      fprev[e] = fk;
+      gprev[e] = gv;
+      continue;
+    }
+    const T df = fk - fprev[e];  // anderson.py:89
+    const T dg = gv - gprev[e];  // anderson.py:90
+    dfn[e] = df;
+    dgn[e] = dg;
+    fprev[e] = fk;
+    gprev[e] = gv;
+    const double dfd = (double)df;
+    dd += dfd * dfd;
+    fd += fkd * dfd;
+#pragma unroll
+    for (int i = 0; i < MW; ++i) {
+      if (i < nw) {
+        const double c = (double)DF[(int64_t)slots.s[i] * n + e];
+        a_dd[i] += dfd * c;
+        a_fd[i] += fkd * c;
+      }
+    }
+  }
+  // block reduction of 2*nw + 3 accumulators, written as this block's partials
+  const int na = 2 * nw + 3;
+  __shared__ double red[kThreads / 32][2 * kMaxMem + 3];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  auto warp_put = [&](int idx, double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[wid][idx] = v;
+  };
+#pragma unroll
+  for (int i = 0; i < MW; ++i) {
+    if (i < nw) {
+      warp_put(i, a_dd[i]);
+      warp_put(nw + 1 + i, a_fd[i]);
+    }
+  }
+  warp_put(nw, dd);
+  warp_put(2 * nw + 1, fd);
+  warp_put(2 * nw + 2, ff);
+  __syncthreads();
+  for (int k = threadIdx.x; k < na; k += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) s += red[w][k];
+    part[(int64_t)blockIdx.x * na + k] = s;
+  }
+}
+
+// sum partials over blocks in fixed order: out[k] = sum_b part[b*na + k]
+__global__ void k_sum_cols(const double* __restrict__ part, int nb, int na,
+                           double* __restrict__ out) {
+  const int k = blockIdx.x;
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) acc += part[(int64_t)b * na + k];
+  const double s = block_sum(acc);
+  if (threadIdx.x == 0) out[k] = s;
+}
+
+// recombination (anderson.py:140-148):
+//   beta == 1: out = G_k - sum_i gamma_i dG_i
+//   else     : out = (1-beta) (p_k - sum gamma_i (dG_i - dF_i)) + beta (G_k - sum gamma_i dG_i)
+//              (sum_i alpha_i x_i = x_k - sum_i gamma_i dx_i, p = G - f)
+template <typename T, int MW>
+__global__ void __launch_bounds__(kThreads)
+    k_aa_step(const T* __restrict__ gk, const T* __restrict__ fk, const T* __restrict__ DF,
+              const T* __restrict__ DG, int64_t n, const Slots slots, int nw, const Coefs gam,
+              double beta, T* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double acc = (double)gk[e];
+    if (beta == 1.0) {
+#pragma unroll
+      for (int i = 0; i < MW; ++i)
+        if (i < nw) acc -= gam.c[i] * (double)DG[(int64_t)slots.s[i] * n + e];
+      out[e] = (T)acc;
+    } else {
+      double cp = acc - (double)fk[e];
+#pragma unroll
+      for (int i = 0; i < MW; ++i)
+        if (i < nw) {
+          const double dg = (double)DG[(int64_t)slots.s[i] * n + e];
+          const double df = (double)DF[(int64_t)slots.s[i] * n + e];
+          acc -= gam.c[i] * dg;
+          cp -= gam.c[i] * (dg - df);
+        }
+      out[e] = (T)((1.0 - beta) * cp + beta * acc);
+    }
+  }
+}
+
+// ---- vector helpers ------------------------------------------------------------
+
+template <typename T>
+__global__ void k_axpby(int64_t n, double a, const T* __restrict__ x, double b,
+                        const T* __restrict__ y, T* __restrict__ z) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (a == 1.0) z[e] = x[e] + (T)b * y[e];  // p - eta g  (anderson.py:322)
+    else z[e] = (T)a * x[e] + (T)b * y[e];
+  }
+}
+
+template <typename T>
+__global__ void k_lerp(int64_t n, const T* __restrict__ x, const T* __restrict__ y, double lam,
+                       T* __restrict__ z) {
+  // z = x + lam (y - x)   (anderson.py:362, 369)
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    z[e] = x[e] + (T)lam * (y[e] - x[e]);
+}
+
+// <g, pbar - p>, <g, ptil - pbar> partials (anderson.py:362-364)
+template <typename T>
+__global__ void k_blend_dots(int64_t n, const T* __restrict__ g, const T* __restrict__ p,
+                             const T* __restrict__ pb, const T* __restrict__ pt,
+                             double* __restrict__ part) {
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double gv = (double)g[e];
+    const double b = (double)pb[e];
+    s0 += gv * (b - (double)p[e]);
+    s1 += gv * ((double)pt[e] - b);
+  }
+  const double r0 = block_sum(s0);
+  __syncthreads();
+  const double r1 = block_sum(s1);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = r0;
+    part[2 * blockIdx.x + 1] = r1;
+  }
+}
+
+// {min, max, max|x|, sum x^2, nonfinite} partials
+template <typename T>
+__global__ void k_stats(int64_t n, const T* __restrict__ x, double* __restrict__ part) {
+  double mn = INFINITY, mx = -INFINITY, ma = 0.0, s2 = 0.0, bad = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double v = (double)x[e];
+    if (!isfinite(v)) {
+      bad += 1.0;
+      continue;
+    }
+    mn = fmin(mn, v);
+    mx = fmax(mx, v);
+    ma = fmax(ma, fabs(v));
+    s2 += v * v;
+  }
+  __shared__ double r[3][kThreads];
+  r[0][threadIdx.x] = mn;
+  r[1][threadIdx.x] = mx;
+  r[2][threadIdx.x] = ma;
+  const double t2 = block_sum(s2);
+  __syncthreads();
+  const double tb = block_sum(bad);
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      r[0][threadIdx.x] = fmin(r[0][threadIdx.x], r[0][threadIdx.x + s]);
+      r[1][threadIdx.x] = fmax(r[1][threadIdx.x], r[1][threadIdx.x + s]);
+      r[2][threadIdx.x] = fmax(r[2][threadIdx.x], r[2][threadIdx.x + s]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double* o = part + 5 * blockIdx.x;
+    o[0] = r[0][0];
+    o[1] = r[1][0];
+    o[2] = r[2][0];
+    o[3] = t2;
+    o[4] = tb;
+  }
+}
+
+int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(kBlocks, (n + kThreads - 1) / kThreads)); }
+
+// exactly rounded sum (Shewchuk partials, as Python's math.fsum)
+double fsum(const std::vector<double>& xs) {
+  std::vector<double> parts;
+  for (double x : xs) {
+    size_t i = 0;
+    for (double y : parts) {
+      if (std::fabs(x) < std::fabs(y)) std::swap(x, y);
+      const double hi = x + y;
+      const double lo = y - (hi - x);
+      if (lo != 0.0) parts[i++] = lo;
+      x = hi;
+    }
+    parts.resize(i);
+    parts.push_back(x);
+  }
+  // sum partials from the top with correct rounding of the final result
+  if (parts.empty()) return 0.0;
+  int n = (int)parts.size() - 1;
+  double hi = parts[n], lo = 0.0;
+  while (n > 0) {
+    const double x = hi;
+    const double y = parts[--n];
+    hi = x + y;
+    const double yr = hi - x;
+    lo = y - yr;
+    if (lo != 0.0) break;
+  }
+  if (n > 0 && ((lo < 0 && parts[n - 1] < 0) || (lo > 0 && parts[n - 1] > 0))) {
+    const double y = lo * 2.0;
+    const double x = hi + y;
+    const double yr = x - hi;
+    if (y == yr) hi = x;
+  }
+  return hi;
+}
+
+}  // namespace
+
+struct sg_aa {
+  int64_t n = 0;
+  int memory = 0;
+  int esz = 8;
+  int device = 0;
+  cudaStream_t stream = 0;
+  void* DF = nullptr;  // memory slots
+  void* DG = nullptr;
+  void* fk = nullptr;  // f_k (after push) = previous f for the next push
+  void* gk = nullptr;  // G_k
+  double* part = nullptr;
+  double* out = nullptr;
+  // window bookkeeping (oldest first)
+  int head = 0;    // ring index of the oldest column
+  int ncols = 0;   // columns in the window
+  int pushes = 0;  // entries in fs (reference len(fs)), capped semantics below
+  std::vector<double> gram;  // memory x memory, window order
+  std::vector<double> bvec;  // <DF_i, f_k>
+  double fk2 = 0.0;
+  // cached weights of the current window
+  bool have_w = false;
+  std::vector<double> gamma, alpha;
+  double resid = 0.0;
+};
+
+namespace {
+
+int slot_of(const sg_aa* a, int pos) { return (a->head + pos) % std::max(1, a->memory); }
+
+double& G(sg_aa* a, int i, int j) { return a->gram[(size_t)i * a->memory + j]; }
+
+void drop_oldest(sg_aa* a) {
+  const int m = a->memory;
+  std::vector<double> g2(a->gram.size(), 0.0);
+  for (int i = 1; i < a->ncols; ++i)
+    for (int j = 1; j < a->ncols; ++j) g2[(size_t)(i - 1) * m + (j - 1)] = a->gram[(size_t)i * m + j];
+  a->gram.swap(g2);
+  for (int i = 1; i < a->ncols; ++i) a->bvec[i - 1] = a->bvec[i];
+  a->head = (a->head + 1) % m;
+  a->ncols -= 1;
+  a->pushes -= 1;  // ps/gs/fs/dgs all pop(0) in the reference (anderson.py:98-103)
+}
+
+// Cholesky R (upper, R^T R = Gram) with the reference's dependence rule: a
+// pivot is zero when rho < 1e-15 max(||a||, 1) (qr.py:47-53) or when it is
+// below the Gram formulation's resolution (rho^2 <= 1e-14 ||a||^2).
+void cholesky(const sg_aa* a, std::vector<double>& R, std::vector<double>& diag) {
+  const int k = a->ncols, m = a->memory;
+  R.assign((size_t)k * k, 0.0);
+  diag.assign(k, 0.0);
+  for (int j = 0; j < k; ++j) {
+    const double ajj = a->gram[(size_t)j * m + j];
+    for (int i = 0; i < j; ++i) {
+      double s = a->gram[(size_t)i * m + j];
+      for (int l = 0; l < i; ++l) s -= R[(size_t)l * k + i] * R[(size_t)l * k + j];
+      R[(size_t)i * k + j] = diag[i] > 0.0 ? s / diag[i] : 0.0;
+    }
+    double s = ajj;
+    for (int l = 0; l < j; ++l) s -= R[(size_t)l * k + j] * R[(size_t)l * k + j];
+    const double nrm = std::sqrt(std::max(ajj, 0.0));
+    double rho = s > 0.0 ? std::sqrt(s) : 0.0;
+    if (rho <= 1e-300 || rho < 1e-15 * std::max(nrm, 1.0) || s <= 1e-14 * ajj) rho = 0.0;
+    diag[j] = rho;
+    R[(size_t)j * k + j] = rho;
+  }
+}
+
+// safeguard (anderson.py:105-112): shed oldest columns while
+// min|diag R| <= 1e-12 ||R||_F
+void safeguard(sg_aa* a) {
+  std::vector<double> R, d;
+  while (a->ncols > 0) {
+    cholesky(a, R, d);
+    double fro2 = 0.0;
+    for (double v : R) fro2 += v * v;
+    const double tol = 1e-12 * std::max(std::sqrt(fro2), 1e-300);
+    if (*std::min_element(d.begin(), d.end()) > tol) break;
+    drop_oldest(a);
+  }
+}
+
+int compute_weights(sg_aa* a) {
+  const int k = a->ncols;
+  if (k == 0 || a->pushes < 2) return fail(SG_ERR_EMPTY, "aa_weights needs at least one stored difference");
+  std::vector<double> R, d;
+  cholesky(a, R, d);
+  // forward solve R^T y = b, back solve R gamma = y  (== solve_triangular(R, Q^T f))
+  std::vector<double> y(k), gmm(k);
+  for (int i = 0; i < k; ++i) {
+    double s = a->bvec[i];
+    for (int l = 0; l < i; ++l) s -= R[(size_t)l * k + i] * y[l];
+    y[i] = s / R[(size_t)i * k + i];
+  }
+  for (int i = k - 1; i >= 0; --i) {
+    double s = y[i];
+    for (int l = i + 1; l < k; ++l) s -= R[(size_t)i * k + l] * gmm[l];
+    gmm[i] = s / R[(size_t)i * k + i];
+  }
+  // residual ||f - A gamma||^2 = ||f||^2 - ||y||^2, clipped to [0, ||f||^2]
+  double y2 = 0.0;
+  for (double v : y) y2 += v * v;
+  const double r2 = std::max(a->fk2 - y2, 0.0);
+  a->resid = std::min(std::sqrt(r2), std::sqrt(a->fk2));
+  // alpha recovery with fsum fix-up (anderson.py:41-52)
+  std::vector<double> al(k + 1);
+  al[0] = gmm[0];
+  for (int i = 1; i < k; ++i) al[i] = gmm[i] - gmm[i - 1];
+  al[k] = 1.0 - gmm[k - 1];
+  for (int it = 0; it < 3; ++it) {
+    const double gap = 1.0 - fsum(al);
+    if (gap == 0.0) break;
+    int arg = 0;
+    for (int i = 1; i <= k; ++i)
+      if (std::fabs(al[i]) > std::fabs(al[arg])) arg = i;
+    al[arg] += gap;
+  }
+  a->gamma = gmm;
+  a->alpha = al;
+  a->have_w = true;
+  return SG_OK;
+}
+
+template <typename T>
+int push_t(sg_aa* a, const void* p, const void* g) {
+  const int first = (a->pushes == 0 || a->memory == 0) ? 1 : 0;
+  Slots sl{};
+  int nw = 0, snew = 0;
+  if (!first) {
+    // a full window drops its oldest column now; the new difference takes its slot
+    if (a->ncols == a->memory) drop_oldest(a);
+    nw = a->ncols;
+    for (int i = 0; i < nw; ++i) sl.s[i] = slot_of(a, i);
+    snew = slot_of(a, nw);
+  }
+  const int nb = grid_for(a->n);
+  const int na = first ? 3 : 2 * nw + 3;
+  T* DF = reinterpret_cast<T*>(a->DF);
+  T* DG = reinterpret_cast<T*>(a->DG);
+  const T* pp = reinterpret_cast<const T*>(p);
+  const T* gg = reinterpret_cast<const T*>(g);
+  T* fk = reinterpret_cast<T*>(a->fk);
+  T* gk = reinterpret_cast<T*>(a->gk);
+  const int mw = std::max(nw, 1);
+#define PUSH(MW) k_aa_push<T, MW><<<nb, kThreads, 0, a->stream>>>(pp, gg, fk, gk, DF, DG, a->n, sl, nw, snew, first, a->part)
+  if (mw <= 4) PUSH(4);
+  else if (mw <= 8) PUSH(8);
+  else if (mw <= 16) PUSH(16);
+  else PUSH(32);
+#undef PUSH
+  k_sum_cols<<<na, 256, 0, a->stream>>>(a->part, nb, na, a->out);
+  count_launch(2);
+  SG_CK(cudaGetLastError());
+  std::vector<double> o(na);
+  SG_CK(cudaMemcpyAsync(o.data(), a->out, na * sizeof(double), cudaMemcpyDeviceToHost, a->stream));
+  SG_CK(cudaStreamSynchronize(a->stream));
+  a->have_w = false;
+  if (first) {
+    // memory 0 keeps only the latest entry; otherwise this is fs[0]
+    a->fk2 = o[2];
+    a->pushes = 1;
+    a->ncols = 0;
+    a->head = 0;
+    return SG_OK;
+  }
+  // oldest-first layout: window positions 0..nw-1 then the new column at nw
+  const int m = a->memory;
+  for (int i = 0; i < nw; ++i) {
+    G(a, i, nw) = o[i];
+    G(a, nw, i) = o[i];
+    a->bvec[i] = o[nw + 1 + i];
+  }
+  G(a, nw, nw) = o[nw];
+  a->bvec[nw] = o[2 * nw + 1];
+  a->fk2 = o[2 * nw + 2];
+  a->ncols = nw + 1;
+  a->pushes += 1;
+  (void)m;
+  safeguard(a);
+  return SG_OK;
+}
+
+template <typename T>
+int step_t(sg_aa* a, double beta, const double* gamma, void* out) {
+  const int k = a->ncols;
+  Slots sl{};
+  Coefs cf{};
+  for (int i = 0; i < k; ++i) {
+    sl.s[i] = slot_of(a, i);
+    cf.c[i] = gamma ? gamma[i] : a->gamma[i];
+  }
+  const int nb = grid_for(a->n);
+  const T* gk = reinterpret_cast<const T*>(a->gk);
+  const T* fk = reinterpret_cast<const T*>(a->fk);
+  const T* DF = reinterpret_cast<const T*>(a->DF);
+  const T* DG = reinterpret_cast<const T*>(a->DG);
+  T* o = reinterpret_cast<T*>(out);
+  const int mw = std::max(k, 1);
+#define STEP(MW) k_aa_step<T, MW><<<nb, kThreads, 0, a->stream>>>(gk, fk, DF, DG, a->n, sl, k, cf, beta, o)
+  if (mw <= 4) STEP(4);
+  else if (mw <= 8) STEP(8);
+  else if (mw <= 16) STEP(16);
+  else STEP(32);
+#undef STEP
+  count_launch();
+  SG_CK(cudaGetLastError());
+  return SG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sg_aa_create(int64_t n, int32_t memory, int32_t dtype, int32_t device, sg_aa** out) {
+  if (!out) return fail(SG_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (n < 1) return fail(SG_ERR_ARG, "rows must be positive");
+  if (memory < 0) return fail(SG_ERR_ARG, "memory must be non-negative");
+  if (memory > kMaxMem) return fail(SG_ERR_ARG, "memory above " + std::to_string(kMaxMem));
+  if (dtype != SG_F32 && dtype != SG_F64) return fail(SG_ERR_ARG, "dtype must be 4 or 8");
+  SG_CK(cudaSetDevice(device));
+  sg_aa* a = new sg_aa();
+  a->n = n;
+  a->memory = memory;
+  a->esz = dtype;
+  a->device = device;
+  const size_t vb = (size_t)n * dtype;
+  const int slots = std::max(memory, 1);
+  cudaError_t e = cudaMalloc(&a->DF, vb * slots);
+  if (e == cudaSuccess) e = cudaMalloc(&a->DG, vb * slots);
+  if (e == cudaSuccess) e = cudaMalloc(&a->fk, vb);
+  if (e == cudaSuccess) e = cudaMalloc(&a->gk, vb);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&a->part, sizeof(double) * kBlocks * (2 * kMaxMem + 3));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&a->out, sizeof(double) * (2 * kMaxMem + 8));
+  if (e != cudaSuccess) {
+    sg_aa_destroy(a);
+    cudaGetLastError();
+    return fail(SG_ERR_OOM, std::string("AA window allocation failed: ") + cudaGetErrorString(e));
+  }
+  a->gram.assign((size_t)slots * slots, 0.0);
+  a->bvec.assign(slots + 1, 0.0);
+  *out = a;
+  return SG_OK;
+}
+
+int sg_aa_destroy(sg_aa* a) {
+  if (!a) return SG_OK;
+  cudaSetDevice(a->device);
+  for (void* p : {a->DF, a->DG, a->fk, a->gk, (void*)a->part, (void*)a->out})
+    if (p) cudaFree(p);
+  delete a;
+  return SG_OK;
+}
+
+int sg_aa_set_stream(sg_aa* a, void* s) {
+  if (!a) return fail(SG_ERR_ARG, "null window");
+  a->stream = reinterpret_cast<cudaStream_t>(s);
+  return SG_OK;
+}
+
+int sg_aa_clear(sg_aa* a) {
+  if (!a) return fail(SG_ERR_ARG, "null window");
+  a->head = a->ncols = a->pushes = 0;
+  std::fill(a->gram.begin(), a->gram.end(), 0.0);
+  a->have_w = false;
+  return SG_OK;
+}
+
+int sg_aa_push(sg_aa* a, const void* p, const void* g) {
+  if (!a || !p || !g) return fail(SG_ERR_ARG, "null argument");
+  SG_CK(cudaSetDevice(a->device));
+  return a->esz == 4 ? push_t<float>(a, p, g) : push_t<double>(a, p, g);
+}
+
+int sg_aa_m_k(sg_aa* a) {
+  if (!a) return 0;
+  return a->memory == 0 ? 0 : std::max(0, a->pushes - 1);
+}
+
+int sg_aa_weights(sg_aa* a, double* gamma, double* alpha, double* resid, int32_t* m_k) {
+  if (!a) return fail(SG_ERR_ARG, "null window");
+  if (sg_aa_m_k(a) == 0) return fail(SG_ERR_EMPTY, "aa_weights needs at least one stored difference");
+  if (!a->have_w) SG_TRY(compute_weights(a));
+  const int k = a->ncols;
+  if (gamma) std::memcpy(gamma, a->gamma.data(), k * sizeof(double));
+  if (alpha) std::memcpy(alpha, a->alpha.data(), (k + 1) * sizeof(double));
+  if (resid) *resid = a->resid;
+  if (m_k) *m_k = k;
+  return SG_OK;
+}
+
+int sg_aa_step(sg_aa* a, double beta, const double* gamma, const double* alpha, void* out) {
+  (void)alpha;
+  if (!a || !out) return fail(SG_ERR_ARG, "null argument");
+  if (a->pushes == 0) return fail(SG_ERR_EMPTY, "aa_step on an empty window");
+  SG_CK(cudaSetDevice(a->device));
+  if (sg_aa_m_k(a) == 0) {
+    // Picard: G_k (anderson.py:136-137)
+    SG_CK(cudaMemcpyAsync(out, a->gk, (size_t)a->n * a->esz, cudaMemcpyDeviceToDevice, a->stream));
+    return SG_OK;
+  }
+  if (!gamma && !a->have_w) SG_TRY(compute_weights(a));
+  return a->esz == 4 ? step_t<float>(a, beta, gamma, out) : step_t<double>(a, beta, gamma, out);
+}
+
+int sg_aa_fk_norm(sg_aa* a, double* out) {
+  if (!a || !out) return fail(SG_ERR_ARG, "null argument");
+  if (a->pushes == 0) return fail(SG_ERR_EMPTY, "empty window");
+  *out = std::sqrt(a->fk2);
+  return SG_OK;
+}
+
+int sg_vec_axpby(int64_t n, int32_t dtype, double a, const void* x, double b, const void* y,
+                 void* z, void* stream) {
+  if (n < 0 || !x || !y || !z) return fail(SG_ERR_ARG, "bad arguments");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (dtype == SG_F32) k_axpby<float><<<grid_for(n), kThreads, 0, s>>>(n, a, (const float*)x, b, (const float*)y, (float*)z);
+  else k_axpby<double><<<grid_for(n), kThreads, 0, s>>>(n, a, (const double*)x, b, (const double*)y, (double*)z);
+  count_launch();
+  SG_CK(cudaGetLastError());
+  return SG_OK;
+}
+
+int sg_vec_lerp(int64_t n, int32_t dtype, const void* x, const void* y, double lam, void* z,
+                void* stream) {
+  if (n < 0 || !x || !y || !z) return fail(SG_ERR_ARG, "bad arguments");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (dtype == SG_F32) k_lerp<float><<<grid_for(n), kThreads, 0, s>>>(n, (const float*)x, (const float*)y, lam, (float*)z);
+  else k_lerp<double><<<grid_for(n), kThreads, 0, s>>>(n, (const double*)x, (const double*)y, lam, (double*)z);
+  count_launch();
+  SG_CK(cudaGetLastError());
+  return SG_OK;
+}
+
+int sg_vec_blend_dots(int64_t n, int32_t dtype, const void* g, const void* p, const void* pbar,
+                      const void* ptil, double* out, void* stream) {
+  if (n < 1 || !g || !p || !pbar || !ptil || !out) return fail(SG_ERR_ARG, "bad arguments");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int nb = grid_for(n);
+  double* part = nullptr;
+  SG_CK(cudaMallocAsync((void**)&part, sizeof(double) * 2 * nb, s));
+  if (dtype == SG_F32) k_blend_dots<float><<<nb, kThreads, 0, s>>>(n, (const float*)g, (const float*)p, (const float*)pbar, (const float*)ptil, part);
+  else k_blend_dots<double><<<nb, kThreads, 0, s>>>(n, (const double*)g, (const double*)p, (const double*)pbar, (const double*)ptil, part);
+  count_launch();
+  std::vector<double> h(2 * nb);
+  SG_CK(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  SG_CK(cudaFreeAsync(part, s));
+  SG_CK(cudaStreamSynchronize(s));
+  double s0 = 0.0, s1 = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    s0 += h[2 * b];
+    s1 += h[2 * b + 1];
+  }
+  out[0] = s0;
+  out[1] = s1;
+  return SG_OK;
+}
+
+int sg_vec_stats(int64_t n, int32_t dtype, const void* x, double* out, void* stream) {
+  if (n < 1 || !x || !out) return fail(SG_ERR_ARG, "bad arguments");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int nb = grid_for(n);
+  double* part = nullptr;
+  SG_CK(cudaMallocAsync((void**)&part, sizeof(double) * 5 * nb, s));
+  if (dtype == SG_F32) k_stats<float><<<nb, kThreads, 0, s>>>(n, (const float*)x, part);
+  else k_stats<double><<<nb, kThreads, 0, s>>>(n, (const double*)x, part);
+  count_launch();
+  std::vector<double> h(5 * nb);
+  SG_CK(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  SG_CK(cudaFreeAsync(part, s));
+  SG_CK(cudaStreamSynchronize(s));
+  double mn = INFINITY, mx = -INFINITY, ma = 0.0, s2 = 0.0, bad = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    mn = std::min(mn, h[5 * b]);
+    mx = std::max(mx, h[5 * b + 1]);
+    ma = std::max(ma, h[5 * b + 2]);
+    s2 += h[5 * b + 3];
+    bad += h[5 * b + 4];
+  }
+  out[0] = mn;
+  out[1] = mx;
+  out[2] = ma;
+  out[3] = std::sqrt(s2);
+  out[4] = bad;
+  return SG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,1373 @@
+// sg_prop.cu -- propagator context, sweep orchestration and the C ABI for
+// forward modelling, FWI gradients and Born/LSRTM (include/seisgpu.h).
+//
+// Reference behaviour reproduced here:
+//   Workspace                 seisopt/wavesim.py:183-214   -> sg_handle + sg_set_*
+//   _forward_sweep            seisopt/wavesim.py:259-304   -> k_forward_step x nt
+//   _adjoint_sweep            seisopt/wavesim.py:307-346   -> k_adjoint_step x nt
+//   fwi_synthetic / misfit    seisopt/gradients.py:98-115, :70-79
+//   fwi_gradient              seisopt/gradients.py:118-155
+//   BornKernel / lsrtm        seisopt/gradients.py:158-277
+//   fold_pad                  seisopt/wavesim.py:135-147   -> k_fold
+// Shots of one call are processed in batches (grid.y = shot), each batch's
+// nt-step loops captured once into CUDA graphs and replayed.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "seisgpu.h"
+#include "sg_common.cuh"
+#include "sg_kernels.cuh"
+
+namespace sg {
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+}  // namespace sg
+
+using namespace sg;
+
+namespace {
+
+constexpr int BX = 64, BY = 4, NY = 8, TH = BY * NY;  // 64 x 32 tiles, 256 threads
+constexpr int RB = BX * BY;                           // receiver threads per block
+constexpr int kSlack = 256;                           // column slack for profile arrays
+
+// ---------------------------------------------------------------------------
+// small kernels
+// ---------------------------------------------------------------------------
+
+// 1/m on the padded grid with edge replication (seisopt/wavesim.py:126-128,200-201)
+template <typename T, typename M>
+__global__ void k_set_inv_m(const M* __restrict__ m, T* __restrict__ inv_m, int nz, int nx,
+                            int nzp, int nxp, int ldx, int top, int left) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (j >= nxp || i >= nzp) return;
+  const int si = min(max(i - top, 0), nz - 1);
+  const int sj = min(max(j - left, 0), nx - 1);
+  inv_m[i * ldx + j] = (T)(1.0 / (double)m[(int64_t)si * nx + sj]);
+}
+
+// edge-replicated, scaled copy onto the padded grid (Born scale -m_r_pad,
+// seisopt/gradients.py:193-194)
+template <typename T, typename M>
+__global__ void k_extend(const M* __restrict__ m, T* __restrict__ out, int nz, int nx, int nzp,
+                         int nxp, int ldx, int top, int left, double scale) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (j >= nxp || i >= nzp) return;
+  const int si = min(max(i - top, 0), nz - 1);
+  const int sj = min(max(j - left, 0), nx - 1);
+  out[i * ldx + j] = (T)(scale * (double)m[(int64_t)si * nx + sj]);
+}
+
+// min(m) and count of (non-finite or <= 0) entries, partials per block
+template <typename M>
+__global__ void k_model_stats(const M* __restrict__ m, int64_t n, double* __restrict__ part) {
+  double mn = INFINITY, bad = 0.0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const double v = (double)m[k];
+    if (!isfinite(v) || v <= 0.0) bad += 1.0;
+    mn = fmin(mn, v);
+  }
+  __shared__ double smin[1024];
+  smin[threadIdx.x] = mn;
+  const double b = block_sum(bad);
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) smin[threadIdx.x] = fmin(smin[threadIdx.x], smin[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = smin[0];
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+// residual, weighted adjoint source and misfit partials
+//   mode 0 (FWI):  ybar = (w_t dt)(f - g), acc w_t (f-g)^2   (seisopt/gradients.py:137-147)
+//   mode 1 (LSRTM): ybar = f - g,          acc (f-g)^2       (seisopt/gradients.py:269-273)
+//   mode 2 (value): no ybar,               acc w_t (f-g)^2   (seisopt/gradients.py:70-79)
+template <typename T>
+__global__ void k_residual(const T* __restrict__ f, const T* __restrict__ g, T* ybar,
+                           int64_t total, int nt, int nrec, double dt, int mode,
+                           double* __restrict__ part) {
+  double acc = 0.0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)((k / nrec) % nt);
+    const T r = f[k] - g[k];
+    const double w = (mode == 1) ? 1.0 : ((n == 0 || n == nt - 1) ? 0.5 : 1.0);
+    acc += w * (double)r * (double)r;
+    if (mode == 0) ybar[k] = (T)(w * dt) * r;
+    else if (mode == 1) ybar[k] = r;
+  }
+  const double s = block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// out[0] += scale * sum(part[0..n))  -- fixed order, one block
+__global__ void k_finish_sum(const double* __restrict__ part, int n, double scale,
+                             double* out) {
+  double acc = 0.0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) acc += part[k];
+  const double s = block_sum(acc);
+  if (threadIdx.x == 0) out[0] += scale * s;
+}
+
+// acc[o] += sum_b img[b][o] over valid padded cells (shot-order sum)
+template <typename T>
+__global__ void k_reduce_images(const T* __restrict__ img, T* __restrict__ acc, int count,
+                                int64_t stride, int nzp, int nxp, int ldx) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (j >= nxp) return;
+  const int o = i * ldx + j;
+  T s = acc[o];
+  for (int b = 0; b < count; ++b) s += img[(int64_t)b * stride + o];
+  acc[o] = s;
+}
+
+// fold_pad: transpose of edge replication (seisopt/wavesim.py:135-147)
+template <typename T>
+__global__ void k_fold(const T* __restrict__ pad, T* __restrict__ out, int nz, int nx,
+                       int nzp, int nxp, int ldx, int top, int left, int accumulate) {
+  const int ix = blockIdx.x * blockDim.x + threadIdx.x;
+  const int iz = blockIdx.y;
+  if (ix >= nx) return;
+  const int r0 = (iz == 0) ? 0 : top + iz;
+  const int r1 = (iz == nz - 1) ? nzp - 1 : top + iz;
+  const int c0 = (ix == 0) ? 0 : left + ix;
+  const int c1 = (ix == nx - 1) ? nxp - 1 : left + ix;
+  T s = T(0);
+  for (int c = c0; c <= c1; ++c) {
+    T col = T(0);
+    for (int r = r0; r <= r1; ++r) col += pad[r * ldx + c];
+    s += col;
+  }
+  const int64_t o = (int64_t)iz * nx + ix;
+  out[o] = accumulate ? out[o] + s : s;
+}
+
+// compact (rows x nxp) <- pitched (rows x ldx)
+template <typename T>
+__global__ void k_unpitch(const T* __restrict__ src, T* __restrict__ dst, int64_t rows,
+                          int nxp, int ldx) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nxp) return;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) dst[r * nxp + j] = src[r * ldx + j];
+}
+
+// pitched <- compact with dtype conversion (gathers/data in and out)
+template <typename T>
+__global__ void k_copy(const T* __restrict__ src, T* __restrict__ dst, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    dst[k] = src[k];
+}
+
+inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// handle
+// ---------------------------------------------------------------------------
+
+struct GraphEntry {
+  cudaGraphExec_t exec;
+  int64_t kernels;
+};
+
+struct sg_handle {
+  sg_desc d{};
+  int esz = 8;
+  int nzp = 0, nxp = 0, ldx = 0;
+  int64_t plane = 0;   // guarded plane (elements)
+  int64_t origin = 0;  // offset of row 0 inside a guarded plane
+  int64_t hplane = 0;  // compact-row history plane nzp*ldx
+  int64_t tail = 0;    // slack after the last plane of a batch buffer
+  int tiles_x = 0, ntiles = 0, rec_blocks = 0;
+  double cz[5] = {0}, cx[5] = {0};
+  cudaStream_t stream = 0;
+  cudaStream_t cap = nullptr;
+
+  // static device data
+  void* inv_m_buf = nullptr;  // plane + tail
+  void* pz_buf = nullptr;
+  void* px_buf = nullptr;
+  void* gscale_buf = nullptr;  // -m_r on the padded grid (Born)
+  int* src_ij = nullptr;
+  void* src_w = nullptr;
+  int* rec_ij = nullptr;
+  void* rec_w = nullptr;
+  int inj_row0 = 0, inj_nrows = 0;
+  int* inj_ptr = nullptr;
+  int* inj_rec = nullptr;
+  void* inj_w = nullptr;
+  std::vector<double> wavelet;
+  bool have_model = false, have_geom = false, have_wavelet = false, have_sponge = false;
+  double src_scale = 1.0;
+
+  // batch buffers
+  int B = 0;              // capacity (shots)
+  int recon = SG_RECON_FULL;
+  int K = 0, ncp = 0;     // checkpoint interval / count
+  int64_t hist_steps = 0; // steps of history held per shot
+  int* bsrc_ij = nullptr;
+  void* bsrc_w = nullptr;
+  void *u0 = nullptr, *u1 = nullptr, *inc = nullptr;
+  void *l0 = nullptr, *l1 = nullptr, *w = nullptr;
+  void* gath = nullptr;
+  void* hist = nullptr;
+  void* ckpt = nullptr;
+  void* img = nullptr;
+  void* acc_img = nullptr;
+  double* part = nullptr;   // reduction partials
+  double* scal = nullptr;   // [0] misfit accumulator, [1..] scratch
+  int npart = 0;
+  double held_bytes = 0.0;
+
+  // Born cache of background histories
+  void* born_hist = nullptr;
+  int born_b0 = -1, born_count = 0;
+
+  std::map<std::string, GraphEntry> graphs;
+};
+
+namespace {
+
+// Guarded buffers are [lead row][shot 0 plane][shot 1 plane]...[tail]; the lead
+// row keeps the (-R, -R) halo read of shot 0 inside the allocation.
+template <typename T>
+T* field(void* base, const sg_handle* h) {  // pointer to row 0 col 0 of shot 0
+  return reinterpret_cast<T*>(base) + h->ldx + h->origin;
+}
+
+size_t span_bytes(const sg_handle* h, int cnt) {  // lead + cnt planes
+  return ((size_t)h->ldx + (size_t)cnt * h->plane) * h->esz;
+}
+
+int dalloc(sg_handle* h, void** p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *p = nullptr;
+    return fail(SG_ERR_OOM, "cudaMalloc(" + std::to_string(bytes) + ") failed: " +
+                                cudaGetErrorString(e));
+  }
+  SG_CK(cudaMemset(*p, 0, bytes));
+  h->held_bytes += (double)bytes;
+  return SG_OK;
+}
+
+void dfree(void** p) {
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+}
+
+void drop_graphs(sg_handle* h) {
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.exec);
+  h->graphs.clear();
+}
+
+void free_batch(sg_handle* h) {
+  drop_graphs(h);
+  void** bufs[] = {(void**)&h->bsrc_ij, &h->bsrc_w, &h->u0, &h->u1, &h->inc, &h->l0, &h->l1,
+                   &h->w, &h->gath, &h->hist, &h->ckpt, &h->img, &h->acc_img,
+                   (void**)&h->part, (void**)&h->scal};
+  for (auto p : bufs) dfree(p);
+  h->B = 0;
+}
+
+// bytes per shot for the batch buffers in a given reconstruction mode
+double per_shot_bytes(const sg_handle* h, int recon, int K, int ncp) {
+  const double e = h->esz;
+  double b = 6.0 * h->plane + (double)h->d.nt * h->d.n_rec + h->hplane;
+  if (recon == SG_RECON_FULL) b += (double)h->d.nt * h->hplane;
+  else b += (double)K * h->hplane + 2.0 * ncp * h->plane;
+  return b * e + 64.0;
+}
+
+int ensure_batch(sg_handle* h) {
+  if (h->B > 0) return SG_OK;
+  const int nt = h->d.nt;
+  size_t free_b = 0, total_b = 0;
+  SG_CK(cudaMemGetInfo(&free_b, &total_b));
+  double budget = h->d.mem_budget_bytes > 0 ? h->d.mem_budget_bytes : 0.9 * (double)free_b;
+  budget -= 4.0 * (h->plane + h->ldx + h->tail) * h->esz + (64 << 20);  // statics + slack
+  int K = h->d.checkpoint_every > 0 ? h->d.checkpoint_every
+                                    : std::max(1, (int)std::ceil(std::sqrt((double)nt)));
+  K = std::min(K, nt);
+  const int ncp = (nt + K - 1) / K;
+  const int want = h->d.batch > 0 ? std::min(h->d.batch, h->d.n_shots) : h->d.n_shots;
+  int recon = h->d.recon;
+  const double full_b = per_shot_bytes(h, SG_RECON_FULL, K, ncp);
+  const double ck_b = per_shot_bytes(h, SG_RECON_CHECKPOINT, K, ncp);
+  if (recon == SG_RECON_AUTO) recon = (full_b * want <= budget) ? SG_RECON_FULL : SG_RECON_CHECKPOINT;
+  const double per = recon == SG_RECON_FULL ? full_b : ck_b;
+  int B = (int)std::min<double>(want, std::floor(budget / per));
+  if (B < 1)
+    return fail(SG_ERR_OOM, "one shot needs " + std::to_string(per / 1e9) +
+                                " GB of device memory; budget " + std::to_string(budget / 1e9));
+  h->B = B;
+  h->recon = recon;
+  h->K = K;
+  h->ncp = ncp;
+  h->hist_steps = recon == SG_RECON_FULL ? nt : K;
+  const size_t e = h->esz;
+  const size_t fb = ((size_t)h->ldx + (size_t)B * h->plane + h->tail) * e;
+  SG_TRY(dalloc(h, (void**)&h->bsrc_ij, (size_t)B * 4 * sizeof(int)));
+  SG_TRY(dalloc(h, &h->bsrc_w, (size_t)B * 4 * e));
+  SG_TRY(dalloc(h, &h->u0, fb));
+  SG_TRY(dalloc(h, &h->u1, fb));
+  SG_TRY(dalloc(h, &h->inc, fb));
+  SG_TRY(dalloc(h, &h->l0, fb));
+  SG_TRY(dalloc(h, &h->l1, fb));
+  SG_TRY(dalloc(h, &h->w, fb));
+  SG_TRY(dalloc(h, &h->gath, (size_t)B * nt * h->d.n_rec * e));
+  SG_TRY(dalloc(h, &h->hist, (size_t)B * h->hist_steps * h->hplane * e));
+  if (recon == SG_RECON_CHECKPOINT)
+    SG_TRY(dalloc(h, &h->ckpt, (size_t)ncp * 2 * span_bytes(h, B)));
+  SG_TRY(dalloc(h, &h->img, (size_t)B * h->hplane * e));
+  SG_TRY(dalloc(h, &h->acc_img, (size_t)h->hplane * e));
+  h->npart = 1184;
+  SG_TRY(dalloc(h, (void**)&h->part, (size_t)h->npart * 2 * sizeof(double)));
+  SG_TRY(dalloc(h, (void**)&h->scal, 16 * sizeof(double)));
+  return SG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernel argument builders + launchers
+// ---------------------------------------------------------------------------
+
+template <typename T>
+FwdArgs<T> fwd_args(const sg_handle* h) {
+  FwdArgs<T> a{};
+  a.inv_m = field<T>(h->inv_m_buf, h);
+  a.pz = reinterpret_cast<const T*>(h->pz_buf) + kGuard;
+  a.px = reinterpret_cast<const T*>(h->px_buf) + kGuard;
+  a.plane = h->plane;
+  a.nzp = h->nzp;
+  a.nxp = h->nxp;
+  a.ldx = h->ldx;
+  a.tiles_x = h->tiles_x;
+  a.ntiles = h->ntiles;
+  a.dt2 = (T)(h->d.dt * h->d.dt);
+  for (int k = 0; k < 5; ++k) {
+    a.cz[k] = (T)h->cz[k];
+    a.cx[k] = (T)h->cx[k];
+  }
+  a.rec_ij = h->rec_ij;
+  a.rec_w = reinterpret_cast<const T*>(h->rec_w);
+  a.nrec = h->d.n_rec;
+  return a;
+}
+
+template <typename T>
+AdjArgs<T> adj_args(const sg_handle* h) {
+  AdjArgs<T> a{};
+  a.inv_m = field<T>(h->inv_m_buf, h);
+  a.pz = reinterpret_cast<const T*>(h->pz_buf) + kGuard;
+  a.px = reinterpret_cast<const T*>(h->px_buf) + kGuard;
+  a.plane = h->plane;
+  a.nzp = h->nzp;
+  a.nxp = h->nxp;
+  a.ldx = h->ldx;
+  a.tiles_x = h->tiles_x;
+  a.ntiles = h->ntiles;
+  a.dt2 = (T)(h->d.dt * h->d.dt);
+  for (int k = 0; k < 5; ++k) {
+    a.cz[k] = (T)h->cz[k];
+    a.cx[k] = (T)h->cx[k];
+  }
+  a.inj_row0 = h->inj_row0;
+  a.inj_nrows = h->inj_nrows;
+  a.inj_ptr = h->inj_ptr;
+  a.inj_rec = h->inj_rec;
+  a.inj_w = reinterpret_cast<const T*>(h->inj_w);
+  return a;
+}
+
+template <typename T>
+void launch_fwd(const sg_handle* h, cudaStream_t s, const FwdArgs<T>& a, int count) {
+  dim3 grid(h->ntiles + (a.gather ? h->rec_blocks : 0), count), block(BX, BY);
+  if (h->d.order == 8) k_forward_step<T, 4, BX, BY, NY><<<grid, block, 0, s>>>(a);
+  else k_forward_step<T, 1, BX, BY, NY><<<grid, block, 0, s>>>(a);
+  count_launch();
+}
+
+template <typename T>
+void launch_adj(const sg_handle* h, cudaStream_t s, const AdjArgs<T>& a, int count) {
+  dim3 grid(h->ntiles, count), block(BX, BY);
+  if (h->d.order == 8) k_adjoint_step<T, 4, BX, BY, NY><<<grid, block, 0, s>>>(a);
+  else k_adjoint_step<T, 1, BX, BY, NY><<<grid, block, 0, s>>>(a);
+  count_launch();
+}
+
+// ---- sweep pieces (enqueue only) --------------------------------------------
+
+struct FwdPlan {
+  bool point = true;        // wavelet point source
+  bool gathers = true;      // sample receivers into h->gath
+  void* hist = nullptr;     // history base (per-shot stride hist_shot, step stride hplane)
+  int64_t hist_shot = 0;
+  int hist_n0 = 0;          // step index stored at slot 0
+  bool hist_mod = false;    // slot = (n - hist_n0) % hist_len (rotating)
+  int hist_len = 0;
+  const void* gsrc = nullptr;  // Born source history (same addressing as hist)
+  int64_t gsrc_shot = 0;
+  int gsrc_n0 = 0;
+  bool gsrc_mod = false;
+  int gsrc_len = 0;
+  bool ckpt_save = false;   // save (u_n, inc_n) at n % K == 0
+  void* fu0 = nullptr;      // field buffers (default u0/u1/inc)
+  void* fu1 = nullptr;
+  void* finc = nullptr;
+};
+
+template <typename T>
+void enq_forward(sg_handle* h, cudaStream_t s, int count, int n0, int n1, const FwdPlan& p) {
+  void* U0 = p.fu0 ? p.fu0 : h->u0;
+  void* U1 = p.fu1 ? p.fu1 : h->u1;
+  void* INC = p.finc ? p.finc : h->inc;
+  FwdArgs<T> a = fwd_args<T>(h);
+  a.inc = field<T>(INC, h);
+  if (p.point) {
+    a.src_ij = h->bsrc_ij;
+    a.src_w = reinterpret_cast<const T*>(h->bsrc_w);
+  }
+  if (p.gsrc) {
+    a.gscale = field<T>(h->gscale_buf, h);
+    a.gsrc_stride = p.gsrc_shot;
+  }
+  a.hist_stride = p.hist_shot;
+  a.gather_stride = (int64_t)h->d.nt * h->d.n_rec;
+  const size_t pb = span_bytes(h, count);
+  const size_t sb = span_bytes(h, h->B);
+  for (int n = n0; n < n1; ++n) {
+    const bool odd = ((n - n0) & 1) != 0;
+    void* cur = odd ? U1 : U0;
+    void* nxt = odd ? U0 : U1;
+    if (p.ckpt_save && n % h->K == 0) {
+      char* slot = (char*)h->ckpt + (size_t)(n / h->K) * 2 * sb;
+      cudaMemcpyAsync(slot, cur, pb, cudaMemcpyDeviceToDevice, s);
+      cudaMemcpyAsync(slot + sb, INC, pb, cudaMemcpyDeviceToDevice, s);
+    }
+    a.u = field<T>(cur, h);
+    a.u_next = field<T>(nxt, h);
+    a.amp = (T)h->wavelet[n];
+    if (p.hist) {
+      const int slot = p.hist_mod ? (n - p.hist_n0) % p.hist_len : (n - p.hist_n0);
+      a.hist = reinterpret_cast<T*>(p.hist) + (int64_t)slot * h->hplane;
+    } else {
+      a.hist = nullptr;
+    }
+    if (p.gsrc) {
+      const int slot = p.gsrc_mod ? (n - p.gsrc_n0) % p.gsrc_len : (n - p.gsrc_n0);
+      a.gsrc = reinterpret_cast<const T*>(p.gsrc) + (int64_t)slot * h->hplane;
+    }
+    a.gather = p.gathers ? reinterpret_cast<T*>(h->gath) + (int64_t)n * h->d.n_rec : nullptr;
+    launch_fwd<T>(h, s, a, count);
+  }
+}
+
+struct AdjPlan {
+  const void* hist = nullptr;  // imaging history (nullptr: no imaging)
+  int64_t hist_shot = 0;
+  int hist_n0 = 0;
+  bool inject = true;          // y from h->gath (scaled residual / data)
+  void* vhist = nullptr;       // optional v store
+  int64_t vhist_shot = 0;
+};
+
+template <typename T>
+void enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, const AdjPlan& p) {
+  AdjArgs<T> a = adj_args<T>(h);
+  a.w = field<T>(h->w, h);
+  a.ybar_stride = (int64_t)h->d.nt * h->d.n_rec;
+  a.hist_stride = p.hist_shot;
+  a.image = p.hist ? reinterpret_cast<T*>(h->img) : nullptr;
+  a.image_stride = h->hplane;
+  a.vhist_stride = p.vhist_shot;
+  const int nt = h->d.nt;
+  for (int n = n_hi - 1; n >= n_lo; --n) {
+    const bool odd = ((nt - 1 - n) & 1) != 0;
+    a.lam = field<T>(odd ? h->l1 : h->l0, h);
+    a.lam_next = field<T>(odd ? h->l0 : h->l1, h);
+    a.ybar = p.inject ? reinterpret_cast<const T*>(h->gath) + (int64_t)n * h->d.n_rec : nullptr;
+    a.hist = p.hist ? reinterpret_cast<const T*>(p.hist) + (int64_t)(n - p.hist_n0) * h->hplane
+                    : nullptr;
+    a.vhist = p.vhist ? reinterpret_cast<T*>(p.vhist) + (int64_t)n * h->hplane : nullptr;
+    launch_adj<T>(h, s, a, count);
+  }
+}
+
+// ---- graph capture / replay ---------------------------------------------------
+
+template <typename F>
+int run_graph(sg_handle* h, const std::string& key, F&& body) {
+  if (!h->d.use_graphs) {
+    body(h->stream);
+    SG_CK(cudaGetLastError());
+    return SG_OK;
+  }
+  auto it = h->graphs.find(key);
+  if (it == h->graphs.end()) {
+    if (!h->cap) SG_CK(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+    const int64_t before = g_launches.load();
+    SG_CK(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+    body(h->cap);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(h->cap, &g);
+    if (e != cudaSuccess)
+      return fail(SG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    const int64_t nk = g_launches.load() - before;  // kernels per replay
+    g_launches.fetch_sub(nk);
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess)
+      return fail(SG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    it = h->graphs.emplace(key, GraphEntry{ex, nk}).first;
+  }
+  SG_CK(cudaGraphLaunch(it->second.exec, h->stream));
+  count_launch(it->second.kernels);
+  return SG_OK;
+}
+
+// ---- model / geometry upload helpers --------------------------------------------
+
+template <typename T>
+int upload_cast(sg_handle* h, void** dst, const double* src, size_t n) {
+  std::vector<T> tmp(n);
+  for (size_t k = 0; k < n; ++k) tmp[k] = (T)src[k];
+  SG_TRY(dalloc(h, dst, n * sizeof(T)));
+  SG_CK(cudaMemcpy(*dst, tmp.data(), n * sizeof(T), cudaMemcpyHostToDevice));
+  return SG_OK;
+}
+
+int check_handle(sg_handle* h, bool need_model = true) {
+  if (!h) return fail(SG_ERR_ARG, "null handle");
+  if (!h->have_sponge || !h->have_geom || !h->have_wavelet)
+    return fail(SG_ERR_STATE, "sponge, geometry and wavelet must be set first");
+  if (need_model && !h->have_model) return fail(SG_ERR_STATE, "model not set");
+  SG_CK(cudaSetDevice(h->d.device));
+  return SG_OK;
+}
+
+int check_range(sg_handle* h, int shot0, int count) {
+  if (shot0 < 0 || count < 1 || shot0 + count > h->d.n_shots)
+    return fail(SG_ERR_ARG, "shot range [" + std::to_string(shot0) + ", " +
+                                std::to_string(shot0 + count) + ") outside [0, " +
+                                std::to_string(h->d.n_shots) + ")");
+  return SG_OK;
+}
+
+// load batch-local source taps for shots [b0, b0+cnt)
+int load_batch_sources(sg_handle* h, int b0, int cnt) {
+  SG_CK(cudaMemcpyAsync(h->bsrc_ij, h->src_ij + (size_t)b0 * 4, (size_t)cnt * 4 * sizeof(int),
+                        cudaMemcpyDeviceToDevice, h->stream));
+  SG_CK(cudaMemcpyAsync(h->bsrc_w, (char*)h->src_w + (size_t)b0 * 4 * h->esz,
+                        (size_t)cnt * 4 * h->esz, cudaMemcpyDeviceToDevice, h->stream));
+  return SG_OK;
+}
+
+int zero_fields(sg_handle* h, bool fwd, bool adj, int cnt) {
+  const size_t b = span_bytes(h, cnt);
+  if (fwd) {
+    SG_CK(cudaMemsetAsync(h->u0, 0, b, h->stream));
+    SG_CK(cudaMemsetAsync(h->u1, 0, b, h->stream));
+    SG_CK(cudaMemsetAsync(h->inc, 0, b, h->stream));
+  }
+  if (adj) {
+    SG_CK(cudaMemsetAsync(h->l0, 0, b, h->stream));
+    SG_CK(cudaMemsetAsync(h->l1, 0, b, h->stream));
+    SG_CK(cudaMemsetAsync(h->w, 0, b, h->stream));
+  }
+  return SG_OK;
+}
+
+template <typename T>
+int residual(sg_handle* h, int cnt, const T* obs, int mode) {
+  const int64_t total = (int64_t)cnt * h->d.nt * h->d.n_rec;
+  const int blocks = std::min<int64_t>(h->npart, cdiv(total, 256));
+  k_residual<T><<<blocks, 256, 0, h->stream>>>(reinterpret_cast<const T*>(h->gath), obs,
+                                               reinterpret_cast<T*>(h->gath), total, h->d.nt,
+                                               h->d.n_rec, h->d.dt, mode, h->part);
+  const double scale = (mode == 1) ? 0.5 : 0.5 * h->d.dt;
+  k_finish_sum<<<1, 1024, 0, h->stream>>>(h->part, blocks, scale, h->scal);
+  count_launch(2);
+  SG_CK(cudaGetLastError());
+  return SG_OK;
+}
+
+template <typename T>
+int reduce_images(sg_handle* h, int cnt) {
+  dim3 grid(cdiv(h->nxp, 128), h->nzp);
+  k_reduce_images<T><<<grid, 128, 0, h->stream>>>(
+      reinterpret_cast<const T*>(h->img), reinterpret_cast<T*>(h->acc_img), cnt, h->hplane,
+      h->nzp, h->nxp, h->ldx);
+  count_launch();
+  SG_CK(cudaGetLastError());
+  return SG_OK;
+}
+
+template <typename T>
+int fold_out(sg_handle* h, void* out, int accumulate) {
+  dim3 grid(cdiv(h->d.nx, 128), h->d.nz);
+  k_fold<T><<<grid, 128, 0, h->stream>>>(reinterpret_cast<const T*>(h->acc_img),
+                                         reinterpret_cast<T*>(out), h->d.nz, h->d.nx, h->nzp,
+                                         h->nxp, h->ldx, h->d.pad_top, h->d.pad_left,
+                                         accumulate);
+  count_launch();
+  SG_CK(cudaGetLastError());
+  return SG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// sweep drivers (typed)
+// ---------------------------------------------------------------------------
+
+template <typename T>
+int do_forward_batch(sg_handle* h, int b0, int cnt, bool store_full_hist_ckpt_mode) {
+  // forward over all steps, gathers into h->gath; in gradient context also
+  // stores the full history (FULL) or checkpoints (CHECKPOINT)
+  SG_TRY(load_batch_sources(h, b0, cnt));
+  SG_TRY(zero_fields(h, true, false, cnt));
+  const int nt = h->d.nt;
+  if (!store_full_hist_ckpt_mode) {
+    SG_TRY(run_graph(h, "fwd_plain/" + std::to_string(cnt), [&](cudaStream_t s) {
+      FwdPlan p;
+      enq_forward<T>(h, s, cnt, 0, nt, p);
+    }));
+    return SG_OK;
+  }
+  if (h->recon == SG_RECON_FULL) {
+    SG_TRY(run_graph(h, "fwd_full/" + std::to_string(cnt), [&](cudaStream_t s) {
+      FwdPlan p;
+      p.hist = h->hist;
+      p.hist_shot = (int64_t)h->hist_steps * h->hplane;
+      enq_forward<T>(h, s, cnt, 0, nt, p);
+    }));
+  } else {
+    SG_TRY(run_graph(h, "fwd_ckpt/" + std::to_string(cnt), [&](cudaStream_t s) {
+      FwdPlan p;
+      p.ckpt_save = true;
+      enq_forward<T>(h, s, cnt, 0, nt, p);
+    }));
+  }
+  return SG_OK;
+}
+
+// adjoint over all steps with imaging against the forward history of the
+// current batch (FULL: stored; CHECKPOINT: segment recompute from checkpoints)
+template <typename T>
+int do_adjoint_batch(sg_handle* h, int cnt, const void* cached_hist, int64_t cached_shot) {
+  SG_TRY(zero_fields(h, false, true, cnt));
+  SG_CK(cudaMemsetAsync(h->img, 0, (size_t)cnt * h->hplane * h->esz, h->stream));
+  const int nt = h->d.nt;
+  if (cached_hist != nullptr || h->recon == SG_RECON_FULL) {
+    const void* hb = cached_hist ? cached_hist : h->hist;
+    const int64_t hs = cached_hist ? cached_shot : (int64_t)h->hist_steps * h->hplane;
+    std::string key = std::string(cached_hist ? "adj_cached/" : "adj_full/") +
+                      std::to_string(cnt) + "/" + std::to_string((uintptr_t)hb);
+    SG_TRY(run_graph(h, key, [&](cudaStream_t s) {
+      AdjPlan p;
+      p.hist = hb;
+      p.hist_shot = hs;
+      enq_adjoint<T>(h, s, cnt, nt, 0, p);
+    }));
+    return SG_OK;
+  }
+  // CHECKPOINT: per segment restore -> forward with segment history -> adjoint
+  SG_TRY(run_graph(h, "adj_ckpt/" + std::to_string(cnt), [&](cudaStream_t s) {
+    const size_t pb = span_bytes(h, cnt);
+    const size_t sb = span_bytes(h, h->B);
+    for (int seg = h->ncp - 1; seg >= 0; --seg) {
+      const int n0 = seg * h->K;
+      const int n1 = std::min(nt, n0 + h->K);
+      char* slot = (char*)h->ckpt + (size_t)seg * 2 * sb;
+      cudaMemcpyAsync(h->u0, slot, pb, cudaMemcpyDeviceToDevice, s);
+      cudaMemcpyAsync(h->inc, slot + sb, pb, cudaMemcpyDeviceToDevice, s);
+      FwdPlan fp;
+      fp.gathers = false;
+      fp.hist = h->hist;
+      fp.hist_shot = (int64_t)h->hist_steps * h->hplane;
+      fp.hist_n0 = n0;
+      enq_forward<T>(h, s, cnt, n0, n1, fp);
+      AdjPlan ap;
+      ap.hist = h->hist;
+      ap.hist_shot = (int64_t)h->hist_steps * h->hplane;
+      ap.hist_n0 = n0;
+      enq_adjoint<T>(h, s, cnt, n1, n0, ap);
+    }
+  }));
+  return SG_OK;
+}
+
+template <typename T>
+int copy_gathers_out(sg_handle* h, void* dst, int cnt) {
+  if (dst == h->gath) return SG_OK;
+  const size_t b = (size_t)cnt * h->d.nt * h->d.n_rec * h->esz;
+  SG_CK(cudaMemcpyAsync(dst, h->gath, b, cudaMemcpyDeviceToDevice, h->stream));
+  return SG_OK;
+}
+
+template <typename T>
+int copy_gathers_in(sg_handle* h, const void* src, int cnt) {
+  const size_t b = (size_t)cnt * h->d.nt * h->d.n_rec * h->esz;
+  SG_CK(cudaMemcpyAsync(h->gath, src, b, cudaMemcpyDeviceToDevice, h->stream));
+  return SG_OK;
+}
+
+template <typename T>
+int fwi_synthetic_t(sg_handle* h, int shot0, int count, void* out) {
+  SG_TRY(ensure_batch(h));
+  const size_t per = (size_t)h->d.nt * h->d.n_rec * h->esz;
+  for (int b0 = shot0; b0 < shot0 + count; b0 += h->B) {
+    const int cnt = std::min(h->B, shot0 + count - b0);
+    SG_TRY(do_forward_batch<T>(h, b0, cnt, false));
+    SG_TRY(copy_gathers_out<T>(h, (char*)out + (size_t)(b0 - shot0) * per, cnt));
+  }
+  SG_CK(cudaGetLastError());
+  return SG_OK;
+}
+
+template <typename T>
+int fwi_misfit_t(sg_handle* h, int shot0, int count, const void* obs, double* misfit) {
+  SG_TRY(ensure_batch(h));
+  SG_CK(cudaMemsetAsync(h->scal, 0, sizeof(double), h->stream));
+  const size_t per = (size_t)h->d.nt * h->d.n_rec * h->esz;
+  for (int b0 = shot0; b0 < shot0 + count; b0 += h->B) {
+    const int cnt = std::min(h->B, shot0 + count - b0);
+    SG_TRY(do_forward_batch<T>(h, b0, cnt, false));
+    SG_TRY(residual<T>(h, cnt, reinterpret_cast<const T*>((const char*)obs + (b0 - shot0) * per),
+                       2));
+  }
+  SG_CK(cudaMemcpyAsync(misfit, h->scal, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  SG_CK(cudaStreamSynchronize(h->stream));
+  return SG_OK;
+}
+
+template <typename T>
+int fwi_gradient_t(sg_handle* h, int shot0, int count, const void* obs, double* misfit,
+                   void* grad, int accumulate) {
+  SG_TRY(ensure_batch(h));
+  SG_CK(cudaMemsetAsync(h->scal, 0, sizeof(double), h->stream));
+  SG_CK(cudaMemsetAsync(h->acc_img, 0, (size_t)h->hplane * h->esz, h->stream));
+  const size_t per = (size_t)h->d.nt * h->d.n_rec * h->esz;
+  for (int b0 = shot0; b0 < shot0 + count; b0 += h->B) {
+    const int cnt = std::min(h->B, shot0 + count - b0);
+    SG_TRY(do_forward_batch<T>(h, b0, cnt, true));
+    SG_TRY(residual<T>(h, cnt, reinterpret_cast<const T*>((const char*)obs + (b0 - shot0) * per),
+                       0));
+    SG_TRY(do_adjoint_batch<T>(h, cnt, nullptr, 0));
+    SG_TRY(reduce_images<T>(h, cnt));
+  }
+  SG_TRY(fold_out<T>(h, grad, accumulate));
+  if (misfit) {
+    SG_CK(cudaMemcpyAsync(misfit, h->scal, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    SG_CK(cudaStreamSynchronize(h->stream));
+  }
+  SG_CK(cudaGetLastError());
+  return SG_OK;
+}
+
+// ---- Born -------------------------------------------------------------------------
+
+template <typename T>
+int set_born_scale(sg_handle* h, const void* m_r) {
+  if (!h->gscale_buf)
+    SG_TRY(dalloc(h, &h->gscale_buf, (size_t)(h->ldx + h->plane + h->tail) * h->esz));
+  dim3 grid(cdiv(h->nxp, 128), h->nzp);
+  k_extend<T, T><<<grid, 128, 0, h->stream>>>(reinterpret_cast<const T*>(m_r),
+                                              field<T>(h->gscale_buf, h), h->d.nz, h->d.nx,
+                                              h->nzp, h->nxp, h->ldx, h->d.pad_top,
+                                              h->d.pad_left, -1.0);
+  count_launch();
+  SG_CK(cudaGetLastError());
+  return SG_OK;
+}
+
+bool born_cached_covers(const sg_handle* h, int b0, int cnt) {
+  return h->born_hist && b0 >= h->born_b0 && b0 + cnt <= h->born_b0 + h->born_count;
+}
+
+template <typename T>
+int born_cache_t(sg_handle* h, int shot0, int count) {
+  SG_TRY(ensure_batch(h));
+  dfree(&h->born_hist);
+  drop_graphs(h);
+  h->born_b0 = -1;
+  h->born_count = 0;
+  const size_t per = (size_t)h->d.nt * h->hplane * h->esz;
+  SG_TRY(dalloc(h, &h->born_hist, per * count));
+  h->born_b0 = shot0;
+  h->born_count = count;
+  const int nt = h->d.nt;
+  for (int b0 = shot0; b0 < shot0 + count; b0 += h->B) {
+    const int cnt = std::min(h->B, shot0 + count - b0);
+    SG_TRY(load_batch_sources(h, b0, cnt));
+    SG_TRY(zero_fields(h, true, false, cnt));
+    void* base = (char*)h->born_hist + (size_t)(b0 - shot0) * per;
+    SG_TRY(run_graph(h, "born_fill/" + std::to_string(cnt) + "/" + std::to_string((uintptr_t)base),
+                     [&](cudaStream_t s) {
+                       FwdPlan p;
+                       p.gathers = false;
+                       p.hist = base;
+                       p.hist_shot = (int64_t)nt * h->hplane;
+                       enq_forward<T>(h, s, cnt, 0, nt, p);
+                     }));
+  }
+  SG_CK(cudaStreamSynchronize(h->stream));
+  return SG_OK;
+}
+
+template <typename T>
+int born_forward_t(sg_handle* h, int shot0, int count, const void* m_r, void* out) {
+  SG_TRY(ensure_batch(h));
+  SG_TRY(set_born_scale<T>(h, m_r));
+  const int nt = h->d.nt;
+  const size_t gper = (size_t)nt * h->d.n_rec * h->esz;
+  for (int b0 = shot0; b0 < shot0 + count; b0 += h->B) {
+    const int cnt = std::min(h->B, shot0 + count - b0);
+    if (born_cached_covers(h, b0, cnt)) {
+      // scattered field driven by the cached a0 history (seisopt/wavesim.py:289-290)
+      SG_TRY(zero_fields(h, true, false, cnt));
+      const void* base = (char*)h->born_hist + (size_t)(b0 - h->born_b0) * nt * h->hplane * h->esz;
+      SG_TRY(run_graph(h, "born_fwd_cached/" + std::to_string(cnt) + "/" +
+                              std::to_string((uintptr_t)base),
+                       [&](cudaStream_t s) {
+                         FwdPlan p;
+                         p.point = false;
+                         p.gsrc = base;
+                         p.gsrc_shot = (int64_t)nt * h->hplane;
+                         enq_forward<T>(h, s, cnt, 0, nt, p);
+                       }));
+    } else {
+      // lock-step: background step writes a0_n into a one-slot buffer, the
+      // scattered step (fields l0/l1/w) consumes it in the same stream order
+      SG_TRY(load_batch_sources(h, b0, cnt));
+      SG_TRY(zero_fields(h, true, true, cnt));
+      SG_TRY(run_graph(h, "born_fwd_lock/" + std::to_string(cnt), [&](cudaStream_t s) {
+        for (int n = 0; n < nt; ++n) {
+          FwdPlan bg;
+          bg.gathers = false;
+          bg.hist = h->hist;
+          bg.hist_shot = (int64_t)h->hist_steps * h->hplane;
+          bg.hist_n0 = n;
+          // alternate the background ping-pong by running one step at a time
+          bg.fu0 = (n & 1) ? h->u1 : h->u0;
+          bg.fu1 = (n & 1) ? h->u0 : h->u1;
+          enq_forward<T>(h, s, cnt, n, n + 1, bg);
+          FwdPlan sc;
+          sc.point = false;
+          sc.gsrc = h->hist;
+          sc.gsrc_shot = (int64_t)h->hist_steps * h->hplane;
+          sc.gsrc_n0 = n;
+          sc.fu0 = (n & 1) ? h->l1 : h->l0;
+          sc.fu1 = (n & 1) ? h->l0 : h->l1;
+          sc.finc = h->w;
+          enq_forward<T>(h, s, cnt, n, n + 1, sc);
+        }
+      }));
+    }
+    SG_TRY(copy_gathers_out<T>(h, (char*)out + (size_t)(b0 - shot0) * gper, cnt));
+  }
+  SG_CK(cudaGetLastError());
+  return SG_OK;
+}
+
+template <typename T>
+int born_adjoint_core(sg_handle* h, int shot0, int count, const void* data, int mode_resid,
+                      const void* d_r, double* value, void* image, int accumulate,
+                      const void* m_r) {
+  // mode_resid: 0 -> data given directly; 1 -> LSRTM: data = L m_r - d_r
+  SG_TRY(ensure_batch(h));
+  SG_CK(cudaMemsetAsync(h->acc_img, 0, (size_t)h->hplane * h->esz, h->stream));
+  SG_CK(cudaMemsetAsync(h->scal, 0, sizeof(double), h->stream));
+  const int nt = h->d.nt;
+  const size_t gper = (size_t)nt * h->d.n_rec * h->esz;
+  for (int b0 = shot0; b0 < shot0 + count; b0 += h->B) {
+    const int cnt = std::min(h->B, shot0 + count - b0);
+    if (mode_resid == 1) {
+      SG_TRY(born_forward_t<T>(h, b0, cnt, m_r, h->gath));
+      // born_forward_t copied gathers onto themselves; form the residual in place
+      SG_TRY(residual<T>(h, cnt, reinterpret_cast<const T*>((const char*)d_r + (b0 - shot0) * gper), 1));
+    } else {
+      SG_TRY(copy_gathers_in<T>(h, (const char*)data + (size_t)(b0 - shot0) * gper, cnt));
+    }
+    if (born_cached_covers(h, b0, cnt)) {
+      const void* base = (char*)h->born_hist + (size_t)(b0 - h->born_b0) * nt * h->hplane * h->esz;
+      SG_TRY(do_adjoint_batch<T>(h, cnt, base, (int64_t)nt * h->hplane));
+    } else if (h->recon == SG_RECON_FULL) {
+      // recompute and store the background history, then image against it
+      SG_TRY(load_batch_sources(h, b0, cnt));
+      SG_TRY(zero_fields(h, true, false, cnt));
+      SG_TRY(run_graph(h, "born_bg_full/" + std::to_string(cnt), [&](cudaStream_t s) {
+        FwdPlan p;
+        p.gathers = false;
+        p.hist = h->hist;
+        p.hist_shot = (int64_t)h->hist_steps * h->hplane;
+        enq_forward<T>(h, s, cnt, 0, nt, p);
+      }));
+      SG_TRY(do_adjoint_batch<T>(h, cnt, nullptr, 0));
+    } else {
+      SG_TRY(load_batch_sources(h, b0, cnt));
+      SG_TRY(zero_fields(h, true, false, cnt));
+      SG_TRY(run_graph(h, "born_bg_ckpt/" + std::to_string(cnt), [&](cudaStream_t s) {
+        FwdPlan p;
+        p.gathers = false;
+        p.ckpt_save = true;
+        enq_forward<T>(h, s, cnt, 0, nt, p);
+      }));
+      SG_TRY(do_adjoint_batch<T>(h, cnt, nullptr, 0));
+    }
+    SG_TRY(reduce_images<T>(h, cnt));
+  }
+  SG_TRY(fold_out<T>(h, image, accumulate));
+  if (value) {
+    SG_CK(cudaMemcpyAsync(value, h->scal, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    SG_CK(cudaStreamSynchronize(h->stream));
+  }
+  SG_CK(cudaGetLastError());
+  return SG_OK;
+}
+
+// ---- single-shot history export (forward_solve / adjoint_solve) ----------------
+
+template <typename T>
+int forward_history_t(sg_handle* h, int shot, void* gather, void* accel) {
+  SG_TRY(ensure_batch(h));
+  const int nt = h->d.nt;
+  void* tmp = nullptr;
+  SG_TRY(dalloc(h, &tmp, (size_t)nt * h->hplane * h->esz));
+  SG_TRY(load_batch_sources(h, shot, 1));
+  SG_TRY(zero_fields(h, true, false, 1));
+  FwdPlan p;
+  p.hist = tmp;
+  p.hist_shot = (int64_t)nt * h->hplane;
+  enq_forward<T>(h, h->stream, 1, 0, nt, p);
+  SG_CK(cudaGetLastError());
+  SG_TRY(copy_gathers_out<T>(h, gather, 1));
+  dim3 grid(cdiv(h->nxp, 128), 4096);
+  k_unpitch<T><<<grid, 128, 0, h->stream>>>(reinterpret_cast<T*>(tmp), reinterpret_cast<T*>(accel),
+                                            (int64_t)nt * h->nzp, h->nxp, h->ldx);
+  count_launch();
+  SG_CK(cudaStreamSynchronize(h->stream));
+  cudaFree(tmp);
+  h->held_bytes -= (double)nt * h->hplane * h->esz;
+  return SG_OK;
+}
+
+template <typename T>
+int adjoint_history_t(sg_handle* h, const void* ybar, void* vout) {
+  SG_TRY(ensure_batch(h));
+  const int nt = h->d.nt;
+  void* tmp = nullptr;
+  SG_TRY(dalloc(h, &tmp, (size_t)nt * h->hplane * h->esz));
+  SG_TRY(copy_gathers_in<T>(h, ybar, 1));
+  SG_TRY(zero_fields(h, false, true, 1));
+  AdjPlan p;
+  p.vhist = tmp;
+  p.vhist_shot = (int64_t)nt * h->hplane;
+  enq_adjoint<T>(h, h->stream, 1, nt, 0, p);
+  SG_CK(cudaGetLastError());
+  dim3 grid(cdiv(h->nxp, 128), 4096);
+  k_unpitch<T><<<grid, 128, 0, h->stream>>>(reinterpret_cast<T*>(tmp), reinterpret_cast<T*>(vout),
+                                            (int64_t)nt * h->nzp, h->nxp, h->ldx);
+  count_launch();
+  SG_CK(cudaStreamSynchronize(h->stream));
+  cudaFree(tmp);
+  h->held_bytes -= (double)nt * h->hplane * h->esz;
+  return SG_OK;
+}
+
+template <typename T>
+int time_kernel_t(sg_handle* h, int which, int count, int reps, float* ms) {
+  SG_TRY(ensure_batch(h));
+  count = std::min(count, h->B);
+  if (which == 0 && h->recon != SG_RECON_FULL && h->hist_steps < 1)
+    return fail(SG_ERR_STATE, "no history buffer");
+  SG_TRY(load_batch_sources(h, 0, count));
+  cudaEvent_t e0, e1;
+  SG_CK(cudaEventCreate(&e0));
+  SG_CK(cudaEventCreate(&e1));
+  const int n = h->d.nt / 2;
+  auto body = [&](cudaStream_t s) {
+    if (which == 0 || which == 2) {
+      FwdPlan p;
+      if (which == 0) {
+        p.hist = h->hist;
+        p.hist_shot = (int64_t)h->hist_steps * h->hplane;
+        p.hist_n0 = n;
+        p.hist_mod = true;
+        p.hist_len = (int)h->hist_steps;
+      }
+      for (int r = 0; r < reps; ++r) enq_forward<T>(h, s, count, n + (r & 1), n + (r & 1) + 1, p);
+    } else {
+      AdjPlan p;
+      p.hist = h->hist;
+      p.hist_shot = (int64_t)h->hist_steps * h->hplane;
+      p.hist_n0 = n;
+      for (int r = 0; r < reps; ++r) enq_adjoint<T>(h, s, count, n + 1, n, p);
+    }
+  };
+  body(h->stream);  // warm-up
+  SG_CK(cudaEventRecord(e0, h->stream));
+  body(h->stream);
+  SG_CK(cudaEventRecord(e1, h->stream));
+  SG_CK(cudaEventSynchronize(e1));
+  float t = 0.f;
+  SG_CK(cudaEventElapsedTime(&t, e0, e1));
+  *ms = t / reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  SG_CK(cudaGetLastError());
+  return SG_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+
+#define SG_DISPATCH(h, fn, ...) \
+  ((h)->esz == 4 ? fn<float>(__VA_ARGS__) : fn<double>(__VA_ARGS__))
+
+extern "C" {
+
+const char* sg_last_error(void) { return sg::g_err.c_str(); }
+int sg_version(void) { return 1; }
+int64_t sg_launch_count(void) { return sg::g_launches.load(); }
+
+int sg_create(const sg_desc* d, sg_handle** out) {
+  if (!d || !out) return fail(SG_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (d->nz < 3 || d->nx < 3) return fail(SG_ERR_ARG, "grid must be at least 3x3");
+  if (d->pad_top < 0 || d->pad_bottom < 0 || d->pad_left < 0 || d->pad_right < 0)
+    return fail(SG_ERR_ARG, "negative pad");
+  if (d->nt < 2) return fail(SG_ERR_ARG, "nt must be at least 2");
+  if (d->n_shots < 1 || d->n_rec < 1) return fail(SG_ERR_ARG, "need sources and receivers");
+  if (d->dtype != SG_F32 && d->dtype != SG_F64) return fail(SG_ERR_ARG, "dtype must be 4 or 8");
+  if (d->order != 2 && d->order != 8) return fail(SG_ERR_ARG, "order must be 2 or 8");
+  if (!(d->dx > 0 && d->dz > 0 && d->dt > 0)) return fail(SG_ERR_ARG, "spacings must be positive");
+  if (d->recon < 0 || d->recon > 2) return fail(SG_ERR_ARG, "bad recon mode");
+  SG_CK(cudaSetDevice(d->device));
+  sg_handle* h = new sg_handle();
+  h->d = *d;
+  h->esz = d->dtype;
+  h->nzp = d->nz + d->pad_top + d->pad_bottom;
+  h->nxp = d->nx + d->pad_left + d->pad_right;
+  h->ldx = ((h->nxp + 4 + 31) / 32) * 32;
+  h->plane = (int64_t)(h->nzp + 2 * kGuard) * h->ldx;
+  h->origin = (int64_t)kGuard * h->ldx;
+  h->hplane = (int64_t)h->nzp * h->ldx;
+  h->tail = (int64_t)(kTileRowsMax + 2 * kGuard + 2) * h->ldx + 1024;
+  h->tiles_x = (h->nxp + BX - 1) / BX;
+  h->ntiles = h->tiles_x * ((h->nzp + TH - 1) / TH);
+  h->rec_blocks = (d->n_rec + RB - 1) / RB;
+  const double rz = 1.0 / (d->dz * d->dz), rx = 1.0 / (d->dx * d->dx);
+  if (d->order == 2) {
+    h->cz[1] = rz;
+    h->cx[1] = rx;
+  } else {
+    const double c8[5] = {-205.0 / 72.0, 8.0 / 5.0, -1.0 / 5.0, 8.0 / 315.0, -1.0 / 560.0};
+    for (int k = 1; k < 5; ++k) {
+      h->cz[k] = c8[k] * rz;
+      h->cx[k] = c8[k] * rx;
+    }
+  }
+  int rc = dalloc(h, &h->inv_m_buf, (size_t)(h->ldx + h->plane + h->tail) * h->esz);
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return SG_OK;
+}
+
+int sg_destroy(sg_handle* h) {
+  if (!h) return SG_OK;
+  cudaSetDevice(h->d.device);
+  free_batch(h);
+  void** bufs[] = {&h->inv_m_buf, &h->pz_buf, &h->px_buf, &h->gscale_buf, (void**)&h->src_ij,
+                   &h->src_w, (void**)&h->rec_ij, &h->rec_w, (void**)&h->inj_ptr,
+                   (void**)&h->inj_rec, &h->inj_w, &h->born_hist};
+  for (auto p : bufs) dfree(p);
+  if (h->cap) cudaStreamDestroy(h->cap);
+  delete h;
+  return SG_OK;
+}
+
+int sg_set_stream(sg_handle* h, void* s) {
+  if (!h) return fail(SG_ERR_ARG, "null handle");
+  h->stream = reinterpret_cast<cudaStream_t>(s);
+  return SG_OK;
+}
+
+int sg_set_sponge(sg_handle* h, const double* pz, const double* px) {
+  if (!h || !pz || !px) return fail(SG_ERR_ARG, "null argument");
+  SG_CK(cudaSetDevice(h->d.device));
+  // guarded profile arrays: kGuard zeros before, generous zero tail after
+  std::vector<double> z(h->nzp + 2 * kGuard + kTileRowsMax + 16, 0.0);
+  std::vector<double> x(h->ldx + 2 * kGuard + kSlack, 0.0);
+  for (int i = 0; i < h->nzp; ++i) z[kGuard + i] = pz[i];
+  for (int j = 0; j < h->nxp; ++j) x[kGuard + j] = px[j];
+  dfree(&h->pz_buf);
+  dfree(&h->px_buf);
+  if (h->esz == 4) {
+    SG_TRY(upload_cast<float>(h, &h->pz_buf, z.data(), z.size()));
+    SG_TRY(upload_cast<float>(h, &h->px_buf, x.data(), x.size()));
+  } else {
+    SG_TRY(upload_cast<double>(h, &h->pz_buf, z.data(), z.size()));
+    SG_TRY(upload_cast<double>(h, &h->px_buf, x.data(), x.size()));
+  }
+  h->have_sponge = true;
+  return SG_OK;
+}
+
+int sg_set_geometry(sg_handle* h, const int32_t* src_rows, const int32_t* src_cols,
+                    const double* src_w, const int32_t* rec_rows, const int32_t* rec_cols,
+                    const double* rec_w, double src_scale) {
+  if (!h || !src_rows || !src_cols || !src_w || !rec_rows || !rec_cols || !rec_w)
+    return fail(SG_ERR_ARG, "null argument");
+  SG_CK(cudaSetDevice(h->d.device));
+  const int S = h->d.n_shots, R = h->d.n_rec;
+  auto in_grid = [&](int r, int c) { return r >= 0 && r < h->nzp && c >= 0 && c < h->nxp; };
+  // sources: (4, S) -> per shot 4 flat offsets, weights * src_scale
+  // (seisopt/wavesim.py:284: sw = src_w * src_scale)
+  std::vector<int> sij(4 * S);
+  std::vector<double> sw(4 * S);
+  for (int s = 0; s < S; ++s)
+    for (int k = 0; k < 4; ++k) {
+      const int r = src_rows[k * S + s], c = src_cols[k * S + s];
+      if (!in_grid(r, c)) return fail(SG_ERR_ARG, "source tap outside padded grid");
+      sij[s * 4 + k] = r * h->ldx + c;
+      sw[s * 4 + k] = src_w[k * S + s] * src_scale;
+    }
+  std::vector<int> rij(4 * R);
+  int rmin = 1 << 30, rmax = -1;
+  for (int e = 0; e < 4 * R; ++e) {
+    const int r = rec_rows[e], c = rec_cols[e];
+    if (!in_grid(r, c)) return fail(SG_ERR_ARG, "receiver tap outside padded grid");
+    rij[e] = r * h->ldx + c;
+    rmin = std::min(rmin, r);
+    rmax = std::max(rmax, r);
+  }
+  // injection CSR over the receiver row band, entries in np.add.at order
+  // (flattened (4, R) index: k-major) -- seisopt/wavesim.py:228-229
+  const int nrows = rmax - rmin + 1;
+  const int ncell = nrows * h->nxp;
+  std::vector<int> cnt(ncell + 1, 0);
+  for (int e = 0; e < 4 * R; ++e) cnt[(rec_rows[e] - rmin) * h->nxp + rec_cols[e] + 1]++;
+  for (int c = 0; c < ncell; ++c) cnt[c + 1] += cnt[c];
+  std::vector<int> fillp(cnt.begin(), cnt.end() - 1), irec(4 * R);
+  std::vector<double> iw(4 * R);
+  for (int e = 0; e < 4 * R; ++e) {
+    const int cell = (rec_rows[e] - rmin) * h->nxp + rec_cols[e];
+    const int at = fillp[cell]++;
+    irec[at] = e % R;
+    iw[at] = rec_w[e];
+  }
+  void** bufs[] = {(void**)&h->src_ij, &h->src_w, (void**)&h->rec_ij, &h->rec_w,
+                   (void**)&h->inj_ptr, (void**)&h->inj_rec, &h->inj_w};
+  for (auto p : bufs) dfree(p);
+  SG_TRY(dalloc(h, (void**)&h->src_ij, sij.size() * sizeof(int)));
+  SG_CK(cudaMemcpy(h->src_ij, sij.data(), sij.size() * sizeof(int), cudaMemcpyHostToDevice));
+  SG_TRY(dalloc(h, (void**)&h->rec_ij, rij.size() * sizeof(int)));
+  SG_CK(cudaMemcpy(h->rec_ij, rij.data(), rij.size() * sizeof(int), cudaMemcpyHostToDevice));
+  SG_TRY(dalloc(h, (void**)&h->inj_ptr, cnt.size() * sizeof(int)));
+  SG_CK(cudaMemcpy(h->inj_ptr, cnt.data(), cnt.size() * sizeof(int), cudaMemcpyHostToDevice));
+  SG_TRY(dalloc(h, (void**)&h->inj_rec, irec.size() * sizeof(int)));
+  SG_CK(cudaMemcpy(h->inj_rec, irec.data(), irec.size() * sizeof(int), cudaMemcpyHostToDevice));
+  if (h->esz == 4) {
+    SG_TRY(upload_cast<float>(h, &h->src_w, sw.data(), sw.size()));
+    SG_TRY(upload_cast<float>(h, &h->rec_w, rec_w, 4 * (size_t)R));
+    SG_TRY(upload_cast<float>(h, &h->inj_w, iw.data(), iw.size()));
+  } else {
+    SG_TRY(upload_cast<double>(h, &h->src_w, sw.data(), sw.size()));
+    SG_TRY(upload_cast<double>(h, &h->rec_w, rec_w, 4 * (size_t)R));
+    SG_TRY(upload_cast<double>(h, &h->inj_w, iw.data(), iw.size()));
+  }
+  h->inj_row0 = rmin;
+  h->inj_nrows = nrows;
+  h->src_scale = src_scale;
+  h->have_geom = true;
+  drop_graphs(h);
+  return SG_OK;
+}
+
+int sg_set_wavelet(sg_handle* h, const double* amp) {
+  if (!h || !amp) return fail(SG_ERR_ARG, "null argument");
+  for (int n = 0; n < h->d.nt; ++n)
+    if (!std::isfinite(amp[n])) return fail(SG_ERR_ARG, "wavelet contains non-finite values");
+  h->wavelet.assign(amp, amp + h->d.nt);
+  h->have_wavelet = true;
+  drop_graphs(h);  // amplitudes are baked into captured launches
+  return SG_OK;
+}
+
+int sg_set_model(sg_handle* h, const void* m, int32_t mdt) {
+  if (!h || !m) return fail(SG_ERR_ARG, "null argument");
+  if (mdt != SG_F32 && mdt != SG_F64) return fail(SG_ERR_ARG, "m dtype must be 4 or 8");
+  SG_CK(cudaSetDevice(h->d.device));
+  if (!h->part) {
+    // model stats need a partials buffer before the batch buffers exist
+    SG_TRY(ensure_batch(h));
+  }
+  const int64_t n = (int64_t)h->d.nz * h->d.nx;
+  const int blocks = std::min<int64_t>(h->npart, cdiv(n, 256));
+  if (mdt == SG_F32)
+    k_model_stats<float><<<blocks, 256, 0, h->stream>>>((const float*)m, n, h->part);
+  else
+    k_model_stats<double><<<blocks, 256, 0, h->stream>>>((const double*)m, n, h->part);
+  count_launch();
+  std::vector<double> part(2 * blocks);
+  SG_CK(cudaMemcpyAsync(part.data(), h->part, part.size() * sizeof(double),
+                        cudaMemcpyDeviceToHost, h->stream));
+  SG_CK(cudaStreamSynchronize(h->stream));
+  double mn = INFINITY, bad = 0.0;
+  for (int b = 0; b < blocks; ++b) {
+    mn = std::min(mn, part[2 * b]);
+    bad += part[2 * b + 1];
+  }
+  if (bad > 0 || !(mn > 0)) {
+    h->have_model = false;
+    return fail(SG_ERR_MODEL, "model is not positive and finite");
+  }
+  // CFL (seisopt/wavesim.py:92-100, 187-193); 8th order: x sqrt(4/6.5016)
+  const double c_max = 1.0 / std::sqrt(mn);
+  double bound = h->d.cfl_safety * std::min(h->d.dx, h->d.dz) / (c_max * std::sqrt(2.0));
+  if (h->d.order == 8) {
+    const double sym = 205.0 / 72.0 + 2.0 * (8.0 / 5.0 + 1.0 / 5.0 + 8.0 / 315.0 + 1.0 / 560.0);
+    bound *= std::sqrt(4.0 / sym);
+  }
+  if (h->d.dt > bound) {
+    h->have_model = false;
+    char buf[256];
+    snprintf(buf, sizeof buf, "dt=%g exceeds stable bound %.6g (c_max=%.6g, safety=%g)", h->d.dt,
+             bound, c_max, h->d.cfl_safety);
+    return fail(SG_ERR_STABILITY, buf);
+  }
+  dim3 grid(cdiv(h->nxp, 128), h->nzp);
+  if (h->esz == 4) {
+    if (mdt == SG_F32)
+      k_set_inv_m<float, float><<<grid, 128, 0, h->stream>>>((const float*)m, field<float>(h->inv_m_buf, h), h->d.nz, h->d.nx, h->nzp, h->nxp, h->ldx, h->d.pad_top, h->d.pad_left);
+    else
+      k_set_inv_m<float, double><<<grid, 128, 0, h->stream>>>((const double*)m, field<float>(h->inv_m_buf, h), h->d.nz, h->d.nx, h->nzp, h->nxp, h->ldx, h->d.pad_top, h->d.pad_left);
+  } else {
+    if (mdt == SG_F32)
+      k_set_inv_m<double, float><<<grid, 128, 0, h->stream>>>((const float*)m, field<double>(h->inv_m_buf, h), h->d.nz, h->d.nx, h->nzp, h->nxp, h->ldx, h->d.pad_top, h->d.pad_left);
+    else
+      k_set_inv_m<double, double><<<grid, 128, 0, h->stream>>>((const double*)m, field<double>(h->inv_m_buf, h), h->d.nz, h->d.nx, h->nzp, h->nxp, h->ldx, h->d.pad_top, h->d.pad_left);
+  }
+  count_launch();
+  SG_CK(cudaGetLastError());
+  h->have_model = true;
+  if (h->born_hist) {  // background histories of the previous model are stale
+    dfree(&h->born_hist);
+    drop_graphs(h);
+    h->born_b0 = -1;
+    h->born_count = 0;
+  }
+  return SG_OK;
+}
+
+int sg_fwi_synthetic(sg_handle* h, int32_t shot0, int32_t count, void* out) {
+  SG_TRY(check_handle(h));
+  SG_TRY(check_range(h, shot0, count));
+  if (!out) return fail(SG_ERR_ARG, "null output");
+  return SG_DISPATCH(h, fwi_synthetic_t, h, shot0, count, out);
+}
+
+int sg_fwi_misfit(sg_handle* h, int32_t shot0, int32_t count, const void* obs, double* misfit) {
+  SG_TRY(check_handle(h));
+  SG_TRY(check_range(h, shot0, count));
+  if (!obs || !misfit) return fail(SG_ERR_ARG, "null argument");
+  return SG_DISPATCH(h, fwi_misfit_t, h, shot0, count, obs, misfit);
+}
+
+int sg_fwi_gradient(sg_handle* h, int32_t shot0, int32_t count, const void* obs, double* misfit,
+                    void* grad, int32_t accumulate) {
+  SG_TRY(check_handle(h));
+  SG_TRY(check_range(h, shot0, count));
+  if (!obs || !grad) return fail(SG_ERR_ARG, "null argument");
+  return SG_DISPATCH(h, fwi_gradient_t, h, shot0, count, obs, misfit, grad, accumulate);
+}
+
+int sg_born_cache(sg_handle* h, int32_t shot0, int32_t count, int32_t enable) {
+  SG_TRY(check_handle(h));
+  if (!enable) {
+    dfree(&h->born_hist);
+    drop_graphs(h);
+    h->born_b0 = -1;
+    h->born_count = 0;
+    return SG_OK;
+  }
+  SG_TRY(check_range(h, shot0, count));
+  return SG_DISPATCH(h, born_cache_t, h, shot0, count);
+}
+
+int sg_born_forward(sg_handle* h, int32_t shot0, int32_t count, const void* m_r, void* out) {
+  SG_TRY(check_handle(h));
+  SG_TRY(check_range(h, shot0, count));
+  if (!m_r || !out) return fail(SG_ERR_ARG, "null argument");
+  return SG_DISPATCH(h, born_forward_t, h, shot0, count, m_r, out);
+}
+
+int sg_born_adjoint(sg_handle* h, int32_t shot0, int32_t count, const void* data, void* image,
+                    int32_t accumulate) {
+  SG_TRY(check_handle(h));
+  SG_TRY(check_range(h, shot0, count));
+  if (!data || !image) return fail(SG_ERR_ARG, "null argument");
+  return SG_DISPATCH(h, born_adjoint_core, h, shot0, count, data, 0, nullptr, nullptr, image,
+                     accumulate, nullptr);
+}
+
+int sg_lsrtm_gradient(sg_handle* h, int32_t shot0, int32_t count, const void* m_r,
+                      const void* d_r, double* value, void* grad, int32_t accumulate) {
+  SG_TRY(check_handle(h));
+  SG_TRY(check_range(h, shot0, count));
+  if (!m_r || !d_r || !grad) return fail(SG_ERR_ARG, "null argument");
+  return SG_DISPATCH(h, born_adjoint_core, h, shot0, count, nullptr, 1, d_r, value, grad,
+                     accumulate, m_r);
+}
+
+int sg_forward_history(sg_handle* h, int32_t shot, void* gather, void* accel) {
+  SG_TRY(check_handle(h));
+  SG_TRY(check_range(h, shot, 1));
+  if (!gather || !accel) return fail(SG_ERR_ARG, "null argument");
+  return SG_DISPATCH(h, forward_history_t, h, shot, gather, accel);
+}
+
+int sg_adjoint_history(sg_handle* h, const void* ybar, void* v) {
+  SG_TRY(check_handle(h));
+  if (!ybar || !v) return fail(SG_ERR_ARG, "null argument");
+  return SG_DISPATCH(h, adjoint_history_t, h, ybar, v);
+}
+
+int sg_query(sg_handle* h, int32_t* batch, int32_t* recon, double* bytes) {
+  if (!h) return fail(SG_ERR_ARG, "null handle");
+  if (batch) *batch = h->B;
+  if (recon) *recon = h->recon;
+  if (bytes) *bytes = h->held_bytes;
+  return SG_OK;
+}
+
+int sg_time_step_kernel(sg_handle* h, int32_t which, int32_t count, int32_t reps, float* ms) {
+  SG_TRY(check_handle(h));
+  if (!ms || reps < 1 || count < 1) return fail(SG_ERR_ARG, "bad arguments");
+  return SG_DISPATCH(h, time_kernel_t, h, which, count, reps, ms);
+}
+
+}  // extern "C"

@@ -1,0 +1,254 @@
+"""GPU parity: libseisgpu (through the package API / C ABI) vs the golden
+vectors of the reference and the pinned CPU oracle.
+
+Tolerances (BASELINE.json north_star): fp64 relative L2 <= 1e-10; fp32
+relative L2 <= 1e-4 per gradient.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from cases import c1, golden, oracle_setup, rel, small_case
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+F64 = 1e-10
+F32 = 1e-4
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _api():
+    from paper_2008_11778_b200 import gradients, wavesim
+    return gradients, wavesim
+
+
+@pytest.mark.parametrize("order", [2, 8])
+@pytest.mark.parametrize("damp_top", [True, False])
+@pytest.mark.parametrize("graphs", [True, False])
+def test_small_case_fp64(order, damp_top, graphs):
+    gradients, wavesim = _api()
+    case = small_case(order, damp_top)
+    g = case["gold"]
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    prop = wavesim.Propagator(grid, geom, wav, cfg, dtype="float64", use_graphs=graphs)
+    prop.set_model(g["m"])
+    syn = prop.synthetic().cpu().numpy()
+    assert rel(syn, g["syn"]) <= F64
+    val, grad = prop.gradient(g["obs"])
+    assert abs(val - float(g["value"])) <= F64 * abs(float(g["value"]))
+    assert rel(grad.cpu().numpy(), g["grad"]) <= F64
+    # misfit-only path (FwiObjective.value)
+    assert abs(prop.misfit(g["obs"]) - float(g["value"])) <= F64 * abs(float(g["value"]))
+    # Born forward / adjoint / LSRTM, recomputed background (no cache)
+    d = prop.born_forward(g["m_r"]).cpu().numpy()
+    assert rel(d, g["born"]) <= F64
+    img = prop.born_adjoint(g["y"]).cpu().numpy()
+    assert rel(img, g["img"]) <= F64
+    lv, lg = prop.lsrtm_gradient(g["m_r"] * 0.5, g["born"])
+    assert abs(lv - float(g["lsrtm_value"])) <= F64 * abs(float(g["lsrtm_value"]))
+    assert rel(lg.cpu().numpy(), g["lsrtm_grad"]) <= F64
+    # and with the background history cached in HBM
+    prop.born_cache()
+    assert rel(prop.born_forward(g["m_r"]).cpu().numpy(), g["born"]) <= F64
+    assert rel(prop.born_adjoint(g["y"]).cpu().numpy(), g["img"]) <= F64
+
+
+@pytest.mark.parametrize("recon", ["full", "checkpoint"])
+def test_reconstruction_modes_bitwise(recon):
+    """Checkpoint recompute reproduces the stored-history gradient bit for bit."""
+    _, wavesim = _api()
+    case = small_case(8, True)
+    g = case["gold"]
+    ref = wavesim.Propagator(case["grid"], case["geometry"], case["wavelet"], case["config"],
+                             dtype="float32", recon="full")
+    ref.set_model(g["m"])
+    v0, g0 = ref.gradient(g["obs"])
+    prop = wavesim.Propagator(case["grid"], case["geometry"], case["wavelet"], case["config"],
+                              dtype="float32", recon=recon, checkpoint_every=37)
+    prop.set_model(g["m"])
+    v1, g1 = prop.gradient(g["obs"])
+    assert prop.query()["recon"] == recon
+    assert v0 == v1
+    assert torch.equal(g0, g1)
+
+
+def test_batches_match_single_launch():
+    _, wavesim = _api()
+    case = c1(8)
+    g = case["gold"]
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    st = oracle_setup(g["m_true"], grid, geom, cfg)
+    obs = np.stack(oracle.fwi_synthetic(st, wav.samples, geom.nt, threads=5))
+    a = wavesim.Propagator(grid, geom, wav, cfg, dtype="float64")
+    b = wavesim.Propagator(grid, geom, wav, cfg, dtype="float64", batch=2)
+    for p in (a, b):
+        p.set_model(g["m_init"])
+    va, ga = a.gradient(obs)
+    vb, gb = b.gradient(obs)
+    assert b.query()["batch"] == 2
+    assert abs(va - vb) <= 1e-14 * abs(va)
+    assert rel(gb.cpu().numpy(), ga.cpu().numpy()) <= 1e-13
+
+
+@pytest.mark.parametrize("order", [2, 8])
+def test_c1_fp64_gradient(order):
+    gradients, _ = _api()
+    case = c1(order)
+    g = case["gold"]
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    from paper_2008_11778_b200.model import VelocityModel
+    obs = gradients.fwi_synthetic(VelocityModel(grid, g["m_true"]), wav, geom, cfg)
+    assert rel(obs[2].samples, g["obs_shot2"]) <= F64
+    ev = gradients.fwi_gradient(VelocityModel(grid, g["m_init"]), obs, wav, geom, cfg)
+    assert abs(ev.value - float(g["value"])) <= F64 * float(g["value"])
+    assert rel(ev.gradient, g["grad"]) <= F64
+
+
+def test_c1_fp32_gradient():
+    """fp32 production path at C1 (|f-g|/|f| ~ 8e-3: the hardest fp32 case)."""
+    gradients, _ = _api()
+    case = c1(8)
+    g = case["gold"]
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    from paper_2008_11778_b200.model import VelocityModel
+    st = oracle_setup(g["m_true"], grid, geom, cfg)
+    obs = np.stack(oracle.fwi_synthetic(st, wav.samples, geom.nt, threads=5))
+    ev = gradients.fwi_gradient(VelocityModel(grid, g["m_init"]), obs, wav, geom, cfg,
+                                dtype="float32")
+    assert abs(ev.value - float(g["value"])) <= F32 * float(g["value"])
+    assert rel(ev.gradient, g["grad"]) <= F32
+
+
+def test_forward_and_adjoint_histories():
+    _, wavesim = _api()
+    case = small_case(8, True)
+    g = case["gold"]
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    st = oracle_setup(g["m"], grid, geom, cfg)
+    tr, hist = oracle.forward_sweep(st, geom.nt, amp=wav.samples, shot=1, keep=True)
+    prop = wavesim.Propagator(grid, geom, wav, cfg, dtype="float64")
+    prop.set_model(g["m"])
+    gg, aa = prop.forward_history(1)
+    assert rel(gg.cpu().numpy(), tr) <= F64
+    assert rel(aa.cpu().numpy(), hist) <= F64
+    y = g["y"][0]
+    _, vh = oracle.adjoint_sweep(st, y, keep_v=True)
+    v = prop.adjoint_history(y).cpu().numpy()
+    assert rel(v, vh) <= F64
+
+
+def test_edge_cases():
+    gradients, wavesim = _api()
+    from paper_2008_11778_b200.model import StabilityError, VelocityModel, make_ricker
+    case = small_case(8, True)
+    g = case["gold"]
+    geom, grid, cfg = case["geometry"], case["grid"], case["config"]
+    zero = make_ricker(12.0, 2e-3, 300, t0=0.08)
+    zero = type(zero)(samples=np.zeros(300), peak_freq=12.0, t0=0.08)
+    prop = wavesim.Propagator(grid, geom, zero, cfg, dtype="float64")
+    prop.set_model(g["m"])
+    assert float(prop.synthetic().abs().max()) == 0.0
+    # observed == synthetic -> zero misfit and zero gradient
+    wav = case["wavelet"]
+    p2 = wavesim.Propagator(grid, geom, wav, cfg, dtype="float64")
+    p2.set_model(g["m"])
+    v, gr = p2.gradient(p2.synthetic())
+    assert v == 0.0 and float(gr.abs().max()) == 0.0
+    # invalid model -> value inf / ValueError; CFL violation -> StabilityError
+    obj = gradients.FwiObjective(grid, list(g["obs"]), wav, geom, cfg)
+    bad = g["m"].ravel().copy()
+    bad[5] = -1.0
+    assert obj.value(bad) == float("inf")
+    with pytest.raises(ValueError):
+        obj.value_and_grad(bad)
+    bad[5] = np.nan
+    assert obj.value(bad) == float("inf")
+    fast = np.full(grid.shape, 1.0 / 9000.0 ** 2)
+    with pytest.raises(StabilityError):
+        gradients.fwi_gradient(VelocityModel(grid, fast), list(g["obs"]), wav, geom, cfg)
+    with pytest.raises(ValueError):
+        gradients.fwi_gradient(VelocityModel(grid, g["m"]), list(g["obs"])[:1], wav, geom, cfg)
+
+
+def test_born_dot_product():
+    """<L x, y> = <x, L^T y> on the GPU, 50 x 100 grid, 2 sources,
+    500 steps."""
+    gradients, wavesim = _api()
+    from paper_2008_11778_b200.model import (AcquisitionGeometry, Grid2D, SimConfig,
+                                             make_ricker)
+    from paper_2008_11778_b200.synthetic import _smooth
+    rng = np.random.default_rng(3)
+    grid = Grid2D(nx=100, nz=50, dx=20.0, dz=20.0)
+    c = np.full(grid.shape, 2000.0)
+    c[20:] = 2500.0
+    c[35:] = 3000.0
+    m = _smooth(1.0 / c ** 2, 4.0)
+    geom = AcquisitionGeometry(((500.0, 20.0), (1500.0, 20.0)),
+                               tuple((x, 40.0) for x in np.linspace(0, 1980, 80)), dt=2e-3,
+                               nt=500)
+    wav = make_ricker(10.0, 2e-3, 500, t0=0.1)
+    for order in (2, 8):
+        prop = wavesim.Propagator(grid, geom, wav, SimConfig(border_width=20, order=order),
+                                  dtype="float64")
+        prop.set_model(m)
+        x = rng.standard_normal(grid.shape) * 1e-8
+        y = rng.standard_normal((2, 500, 80))
+        lx = prop.born_forward(x).cpu().numpy()
+        lty = prop.born_adjoint(y).cpu().numpy()
+        a, b = float(np.sum(lx * y)), float(np.sum(x * lty))
+        assert abs(a - b) / (np.linalg.norm(lx) * np.linalg.norm(y)) <= 1e-12
+
+
+def test_aa_window_matches_reference_sequence():
+    from paper_2008_11778_b200 import anderson
+    g = golden("aa_window")
+    n, memory = int(g["n"]), int(g["memory"])
+    win = anderson.AAWindow(n, memory, dtype="float64")
+    for k in range(len(g["ps"])):
+        win.push(g["ps"][k], g["gs"][k])
+        assert win.m_k == int(g["m_k"][k]), k
+        if win.m_k:
+            w = anderson.aa_weights(win)
+            mk = win.m_k
+            assert np.allclose(w.gamma, g["gamma"][k][:mk], rtol=1e-10, atol=1e-12)
+            assert np.allclose(w.alpha, g["alpha"][k][:mk + 1], rtol=1e-10, atol=1e-12)
+            assert math_isclose(w.residual_norm, float(g["resid"][k]), 1e-7)
+            assert rel(anderson.aa_step(win, 1.0, w), g["step1"][k]) <= F64
+            assert rel(anderson.aa_step(win, 0.5, w), g["step_half"][k]) <= F64
+        else:
+            assert rel(anderson.aa_step(win), g["step1"][k]) == 0.0
+
+
+def math_isclose(a, b, tol):
+    return abs(a - b) <= tol * max(abs(b), 1e-300)
+
+
+def test_minimize_aa_trajectory_fp64():
+    """GPU objective + GPU AA reproduce the reference minimize_aa run."""
+    gradients, _ = _api()
+    from paper_2008_11778_b200 import anderson
+    gold = golden("aa_fwi_small")
+    case = small_case(8, True)
+    g = case["gold"]
+    obj = gradients.FwiObjective(case["grid"], list(g["obs"]), case["wavelet"],
+                                 case["geometry"], case["config"])
+    res = anderson.minimize_aa(obj, g["m"].ravel(), memory=3, max_iters=8)
+    rows = np.array([[r.iteration, r.objective, r.grad_norm, r.grad_evals, r.obj_evals, r.step]
+                     for r in res.report.rows])
+    assert rows.shape == gold["rows"].shape
+    assert np.array_equal(rows[:, [0, 3, 4, 5]], gold["rows"][:, [0, 3, 4, 5]])
+    assert np.allclose(rows[:, 1], gold["rows"][:, 1], rtol=1e-9)
+    assert rel(res.p, gold["final"]) <= F64
+    assert abs(res.extras["eta"] - float(gold["eta"])) <= 1e-12 * float(gold["eta"])
+    # AA(0) == steepest descent
+    obj0 = gradients.FwiObjective(case["grid"], list(g["obs"]), case["wavelet"],
+                                  case["geometry"], case["config"])
+    r0 = anderson.minimize_aa(obj0, g["m"].ravel(), memory=0, max_iters=3)
+    assert rel(r0.p, gold["sd_final"]) <= F64
