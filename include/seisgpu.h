@@ -66,7 +66,8 @@ typedef struct sg_desc {
   int32_t checkpoint_every;          /* CHECKPOINT interval, 0 = auto (~sqrt(nt)) */
   int32_t device;                    /* CUDA ordinal */
   int32_t use_graphs;                /* capture time loops in CUDA graphs (1) */
-  int32_t reserved[4];
+  int32_t group;                     /* shots per CTA group, 0 = auto */
+  int32_t reserved[3];
   double dx, dz, dt;                 /* metres, seconds */
   double cfl_safety;                 /* SimConfig.cfl_safety, seisopt/wavesim.py:57 */
   double mem_budget_bytes;           /* 0 = 90% of free device memory */

@@ -1,248 +1,370 @@
-// sg_kernels.cuh -- sm_100a time-step kernels for the damped-leapfrog acoustic
+// sg_kernels.cuh -- sm_100a time-step kernel for the damped-leapfrog acoustic
 // propagator of seisopt (seisopt/wavesim.py:259-346), re-designed for B200.
 //
-// Memory layout ("guarded plane", one per shot):
-//   rows  -4 .. nzp+3 (4 zero guard rows top and bottom), row pitch ldx >= nxp+4
-//   (multiple of 32 elements), so every stencil read of a valid cell lands on
-//   either a real cell or a zero cell: the reference's zero-Dirichlet exterior
-//   (seisopt/wavesim.py:216-223) costs no branches.  Columns nxp..ldx-1 are
-//   zero; the left halo of column 0 wraps into the previous row's zero tail.
-//   Field pointers passed to kernels point at row 0, column 0 of shot 0;
-//   shot b lives at +b*plane.
+// Memory layout ("guarded plane", one per shot): rows -4 .. nzp+3 (4 zero
+// guard rows top and bottom) with row pitch ldx >= nxp+4 (multiple of 32
+// elements); buffers are [lead row][shot 0 plane][shot 1 plane]...[tail].
+// Columns nxp..ldx-1 stay zero.  Field pointers point at row 0 col 0 of shot 0.
 //
-// Recursion (algebraically identical to the reference; SURVEY s7 hard part 4):
-//   forward  a_n  = inv_m (L u_n [+ g_n s]) [+ amp_n w_k inv_m at source taps]
-//            inc_{n+1} = d (inc_n + dt^2 a_n),  u_{n+1} = d u_n + inc_{n+1}
-//     (reference: u_{n+1} = d (2 u_n - p_n + dt^2 a_n), p_{n+1} = d u_n, with
-//      inc_n = u_n - p_n).
-//   adjoint  v_n  = dt^2 inv_m d lam_{n+1}
-//            w_n  = d w_{n+1} + L v_n + R^T y_n,  lam_n = d lam_{n+1} + w_n
-//     (reference seisopt/wavesim.py:331-341 with w_n = lam_n - d lam_{n+1}),
-//            image -= a_n v_n  (seisopt/wavesim.py:342-343).
-//   L is applied in difference form sum_k c_k ((u_{+k}-u) + (u_{-k}-u)), which
-//   equals the reference stencil because c_0 = -2 sum_{k>0} c_k.
+// One CTA owns a 64 x 32 tile for a GROUP of G shots.  The halo'd field tile
+// (72 x 40) of each shot is brought into shared memory by TMA
+// (cp.async.bulk.tensor.2d, out-of-bounds zero fill == the reference's
+// zero-Dirichlet exterior, seisopt/wavesim.py:216-223), double-buffered so
+// shot k+1 streams in while shot k computes.  Per-cell model data (1/m,
+// sponge factor) stay in registers across the group; each thread owns 8
+// consecutive rows of one column and keeps the vertical stencil window in
+// registers (z-marching inside the tile), so a cell costs ~10 shared loads.
+//
+// Forward (FWD) and adjoint (ADJ) share the kernel shape:
+//   FWD  a_n = inv_m (L u_n [+ g_n s]) [+ amp_n w_k inv_m at the source taps]
+//        inc_{n+1} = d (inc_n + dt^2 a_n),   u_{n+1} = d u_n + inc_{n+1}
+//        (reference: u_{n+1} = d (2 u_n - p_n + dt^2 a_n), p_{n+1} = d u_n,
+//         with inc_n = u_n - p_n -- the increment form keeps fp32 accurate)
+//   ADJ  state V_n = v_n = dt^2 inv_m d lam_{n+1} (seisopt/wavesim.py:331-333)
+//        w_n = d w_{n+1} + L V_n + R^T y_n,   V_{n-1} = d V_n + (dt^2 inv_m d) w_n
+//        image -= a_n V_n                       (seisopt/wavesim.py:342-343)
+//        (reference lam_n = L v_n + 2 d lam_{n+1} + d pbar + R^T y with
+//         w_n = lam_n - d lam_{n+1}; algebraically identical, exact transpose)
+//   L is applied in difference form sum_k c_k ((u_{+k}-u) + (u_{-k}-u)),
+//   identical to the reference stencil because c_0 = -2 sum_{k>0} c_k.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace sg {
 
-constexpr int kGuard = 4;       // zero guard rows above/below each plane
+constexpr int kGuard = 4;         // zero guard rows above/below each plane
 constexpr int kTileRowsMax = 64;  // tail padding covers tiles up to this height
+constexpr int kBX = 64, kBY = 4, kNY = 8, kTH = kBY * kNY;  // 64 x 32 tile, 256 threads
+// TMA halo boxes are always kHalo wide (the 8th-order radius); the 2nd-order
+// stencil reads the inner ring only.  72 x 40 boxes keep every TMA row a
+// multiple of 16 B for fp32 and fp64.
+constexpr int kHalo = 4;
 
 template <typename T>
-struct FwdArgs {
-  const T* u;        // u_n     (field base, shot 0 row 0 col 0)
-  T* u_next;         // u_{n+1}
-  T* inc;            // increment state, updated in place
-  const T* inv_m;    // 1/m on the padded grid (single plane)
-  const T* pz;       // sponge profile rows (index i)
-  const T* px;       // sponge profile cols (index j)
-  int64_t plane;     // per-shot stride of field buffers (elements)
+struct StepArgs {
+  // TMA descriptors (3-D views {ldx, rows, planes}; see sg_prop.cu tmap_*)
+  CUtensorMap f_halo[2];  // field buffers, box = halo'd tile (load)
+  CUtensorMap f_tile[2];  // field buffers, box = tile (store)
+  CUtensorMap s_tile;     // state buffer (inc / w), box = tile (load + store)
+  CUtensorMap h_tile;     // history buffer {ldx, nzp, shots*steps}, box = tile
+  T* f[2];                // field buffers (row 0, col 0, shot 0)
+  T* state;               // inc (forward) / w (adjoint), updated in place
+  int cur;                // read f[cur], write f[cur ^ 1]
+  const T* inv_m;         // 1/m on the padded grid (single plane)
+  const T* pz;            // sponge profile, rows
+  const T* px;            // sponge profile, cols
+  int64_t plane;          // per-shot stride of field/state buffers
   int nzp, nxp, ldx, tiles_x, ntiles;
+  int count, G;           // shots in this launch, shots per CTA group
   T dt2;
-  T cz[5], cx[5];    // stencil weights, index k = 1..R used
-  // point source: 4 taps per shot (flat offsets i*ldx+j), weights * src_scale
-  const int* src_ij; // nullptr -> no point source
-  const T* src_w;
-  T amp;             // wavelet[n]
-  // Born grid source: a0_n (per shot stride gsrc_stride) times gscale (plane)
-  const T* gsrc;
+  T cz[5], cx[5];         // stencil weights k = 1..R
+  int hist_on;            // FWD: store history; ADJ: image against history
+  int hist_steps, hist_slot;  // history plane of shot b at this step: b*hist_steps + slot
+  T* hist;                // history base (plain stores of the forward)
+  int64_t hplane;         // history plane stride nzp*ldx
+  // ---- forward --------------------------------------------------------------
+  const int* src_rc;      // (count, 4, 2) tap rows/cols; nullptr: no point source
+  const T* src_w;         // (count, 4) weights * src_scale
+  T amp;                  // wavelet[n]
+  const T* gsrc;          // Born source a0_n (per-shot stride gsrc_stride)
   int64_t gsrc_stride;
-  const T* gscale;
-  // acceleration history store for this step (per shot stride hist_stride)
-  T* hist;
-  int64_t hist_stride;
-  // receiver sampling (gathers for this step: gather + b*gather_stride + r)
-  const int* rec_ij;  // (4, nrec)
-  const T* rec_w;     // (4, nrec)
-  int nrec;
-  T* gather;
+  const T* gscale;        // -m_r on the padded grid
+  const int* rec_ij;      // (4, nrec) flat offsets
+  const T* rec_w;         // (4, nrec)
+  int nrec, rec_blocks;   // receiver blocks per group
+  T* gather;              // gathers at this step (+ b*gather_stride + r)
   int64_t gather_stride;
-};
-
-template <typename T>
-struct AdjArgs {
-  const T* lam;       // lam_{n+1} (adjoint field)
-  T* lam_next;        // lam_n
-  T* w;               // increment state, in place
-  const T* inv_m;
-  const T* pz;
-  const T* px;
-  int64_t plane;
-  int nzp, nxp, ldx, tiles_x, ntiles;
-  T dt2;
-  T cz[5], cx[5];
-  // receiver injection (CSR over cells of rows [inj_row0, inj_row0+inj_nrows))
+  // ---- adjoint --------------------------------------------------------------
   int inj_row0, inj_nrows;
-  const int* inj_ptr;  // (inj_nrows*nxp + 1)
-  const int* inj_rec;  // receiver index per entry
-  const T* inj_w;      // weight per entry
-  const T* ybar;       // adjoint data at this step: ybar + b*ybar_stride + r
+  const int* inj_ptr;     // CSR over cells of the receiver row band
+  const int* inj_rec;
+  const T* inj_w;
+  const T* ybar;          // adjoint data at this step (+ b*ybar_stride + r)
   int64_t ybar_stride;
-  // imaging: image[b] -= hist[b] * v   (hist per shot stride hist_stride)
-  const T* hist;
-  int64_t hist_stride;
-  T* image;
+  T* image;               // per-group image planes (stride image_stride)
   int64_t image_stride;
-  // optional v-history store (adjoint_solve keep_v)
-  T* vhist;
+  T* vhist;               // optional v history (adjoint_solve keep_v)
   int64_t vhist_stride;
 };
 
-// ----------------------------------------------------------------------------
-// forward step
-// ----------------------------------------------------------------------------
-template <typename T, int R, int BX, int BY, int NY>
-__global__ void __launch_bounds__(BX* BY)
-    k_forward_step(const FwdArgs<T> a) {
-  constexpr int TH = BY * NY;
-  constexpr int SW = BX + 2 * R;
-  constexpr int SH = TH + 2 * R;
-  __shared__ T s[SH][SW];
+// ---- PTX helpers -----------------------------------------------------------
 
-  const int b = blockIdx.y;
-  const int tid = threadIdx.y * BX + threadIdx.x;
-  const T* __restrict__ u = a.u + (int64_t)b * a.plane;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
 
-  if ((int)blockIdx.x >= a.ntiles) {
-    // receiver sampling blocks: gather[n, r] = sum_k w_k u_n[tap_k]
-    // (seisopt/wavesim.py:225-226, sampled before the update, :287)
-    const int r = ((int)blockIdx.x - a.ntiles) * (BX * BY) + tid;
-    if (a.gather != nullptr && r < a.nrec) {
-      T g = a.rec_w[r] * u[a.rec_ij[r]];
-#pragma unroll
-      for (int k = 1; k < 4; ++k) g += a.rec_w[k * a.nrec + r] * u[a.rec_ij[k * a.nrec + r]];
-      a.gather[(int64_t)b * a.gather_stride + r] = g;
-    }
-    return;
-  }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
 
-  const int tzi = blockIdx.x / a.tiles_x;
-  const int txi = blockIdx.x - tzi * a.tiles_x;
-  const int i0 = tzi * TH;
-  const int j0 = txi * BX;
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
 
-  // stage u_n tile + halo (guard layout: no bounds checks)
-  const T* __restrict__ src = u + (int64_t)(i0 - R) * a.ldx + (j0 - R);
-#pragma unroll 4
-  for (int idx = tid; idx < SH * SW; idx += BX * BY) {
-    const int r = idx / SW;
-    const int c = idx - r * SW;
-    s[r][c] = __ldg(src + (int64_t)r * a.ldx + c);
-  }
-  __syncthreads();
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
-  const int j = j0 + threadIdx.x;
-  if (j >= a.nxp) return;
-  const int jj = threadIdx.x + R;
-  const T pxj = a.px[j];
-  int sij[4];
-  T sw[4];
-  const bool has_src = a.src_ij != nullptr;
-  if (has_src) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      sij[k] = a.src_ij[b * 4 + k];
-      sw[k] = a.src_w[b * 4 + k];
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < NY; ++q) {
-    const int ii = threadIdx.y + q * BY + R;
-    const int i = i0 + ii - R;
-    if (i >= a.nzp) break;
-    const T uc = s[ii][jj];
-    T lz = T(0), lx = T(0);
-#pragma unroll
-    for (int k = 1; k <= R; ++k) {
-      lz += a.cz[k] * ((s[ii - k][jj] - uc) + (s[ii + k][jj] - uc));
-      lx += a.cx[k] * ((s[ii][jj - k] - uc) + (s[ii][jj + k] - uc));
-    }
-    T lap = lz + lx;
-    const int o = i * a.ldx + j;
-    const T im = a.inv_m[o];
-    if (a.gsrc != nullptr) lap += a.gsrc[(int64_t)b * a.gsrc_stride + o] * a.gscale[o];
-    T acc = lap * im;
-    if (has_src) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (o == sij[k]) acc += a.amp * sw[k] * im;
-    }
-    if (a.hist != nullptr) a.hist[(int64_t)b * a.hist_stride + o] = acc;
-    const T d = a.pz[i] * pxj;
-    const int64_t fo = (int64_t)b * a.plane + o;
-    const T inc = d * (a.inc[fo] + a.dt2 * acc);
-    a.inc[fo] = inc;
-    a.u_next[fo] = d * uc + inc;
-  }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra.uni DONE_%=;\n"
+      "bra.uni WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int x,
+                                             int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          map),
+      "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_wait0() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// shared-memory plan of one CTA (element counts; every region 128-B aligned):
+// two stages of {halo'd field tile, state tile[, history tile (adjoint)]}
+template <typename T, int R, bool ADJ>
+struct Smem {
+  static constexpr int SW = kBX + 2 * kHalo;
+  static constexpr int SH = kTH + 2 * kHalo;
+  static constexpr int A = 128 / (int)sizeof(T);  // elements per 128 B
+  static constexpr int HALO = ((SW * SH + A - 1) / A) * A;
+  static constexpr int TILE = kBX * kTH;           // multiple of 128 B
+  static constexpr int STAGE = HALO + (ADJ ? 2 : 1) * TILE;
+  static constexpr int BYTES = 2 * STAGE * (int)sizeof(T);
+};
+
+template <typename T, int R, bool ADJ>
+__host__ __device__ constexpr int step_smem_bytes() {
+  return Smem<T, R, ADJ>::BYTES;
 }
 
 // ----------------------------------------------------------------------------
-// adjoint step with fused receiver injection and imaging condition
+// the step kernel
 // ----------------------------------------------------------------------------
-template <typename T, int R, int BX, int BY, int NY>
-__global__ void __launch_bounds__(BX* BY)
-    k_adjoint_step(const AdjArgs<T> a) {
-  constexpr int TH = BY * NY;
-  constexpr int SW = BX + 2 * R;
-  constexpr int SH = TH + 2 * R;
-  __shared__ T s[SH][SW];  // v_n = dt^2 inv_m d lam_{n+1} on tile + halo
+// FL_* feature flags (compile-time; dead paths vanish from the SASS)
+constexpr int FL_HIST = 1;    // FWD: store a_n; ADJ: image against a_n
+constexpr int FL_GSRC = 2;    // FWD: Born grid source a0_n * gscale
+constexpr int FL_VHIST = 4;   // ADJ: store v_n (adjoint_solve keep_v)
+constexpr int FL_GATHER = 8;  // FWD: receiver sampling blocks present
 
-  const int b = blockIdx.y;
-  const int tid = threadIdx.y * BX + threadIdx.x;
+template <typename T, int R, bool ADJ, int FL>
+__global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? 3 : 2)
+    k_step(const __grid_constant__ StepArgs<T> a) {
+  using SM = Smem<T, R, ADJ>;
+  constexpr int SW = SM::SW;
+  constexpr int NCOL = kNY + 2 * R;
+  constexpr int HO = kHalo - R;  // offset of the radius-R window inside the halo box
+  constexpr bool HIST = (FL & FL_HIST) != 0;
+  constexpr bool GSRC = !ADJ && (FL & FL_GSRC) != 0;
+  constexpr bool VHIST = ADJ && (FL & FL_VHIST) != 0;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* sbase = reinterpret_cast<T*>(smem_raw);
+  __shared__ __align__(8) uint64_t bar[2];
+
+  const int tid = threadIdx.y * kBX + threadIdx.x;
+  const int grp = blockIdx.y;
+  const int b0 = grp * a.G;
+  const int nb = min(a.G, a.count - b0);
+
+  if constexpr (!ADJ && (FL & FL_GATHER) != 0) {
+    if ((int)blockIdx.x >= a.ntiles) {
+      // receiver sampling for this group's shots: gather[n, r] = sum_k w_k u_n[tap_k]
+      // (seisopt/wavesim.py:225-226, sampled before the update, :287)
+      const T* __restrict__ u = a.f[a.cur];
+      const int total = nb * a.nrec;
+      for (int e = ((int)blockIdx.x - a.ntiles) * (kBX * kBY) + tid; e < total;
+           e += a.rec_blocks * (kBX * kBY)) {
+        const int bb = b0 + e / a.nrec;
+        const int r = e - (e / a.nrec) * a.nrec;
+        const T* ub = u + (int64_t)bb * a.plane;
+        T g = a.rec_w[r] * ub[a.rec_ij[r]];
+#pragma unroll
+        for (int k = 1; k < 4; ++k) g += a.rec_w[k * a.nrec + r] * ub[a.rec_ij[k * a.nrec + r]];
+        a.gather[(int64_t)bb * a.gather_stride + r] = g;
+      }
+      return;
+    }
+  }
+
   const int tzi = blockIdx.x / a.tiles_x;
   const int txi = blockIdx.x - tzi * a.tiles_x;
-  const int i0 = tzi * TH;
-  const int j0 = txi * BX;
-  const T* __restrict__ lam = a.lam + (int64_t)b * a.plane;
+  const int i0 = tzi * kTH;
+  const int j0 = txi * kBX;
+  constexpr bool LOAD_HIST = ADJ && HIST;
 
-#pragma unroll 4
-  for (int idx = tid; idx < SH * SW; idx += BX * BY) {
-    const int r = idx / SW;
-    const int c = idx - r * SW;
-    const int i = i0 - R + r;
-    const int j = j0 - R + c;
-    const int o = i * a.ldx + j;
-    const T d = a.pz[i] * a.px[j];
-    s[r][c] = ((d * __ldg(lam + o)) * __ldg(a.inv_m + o)) * a.dt2;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
   }
   __syncthreads();
+  auto issue = [&](int k) {
+    const int s = k & 1;
+    T* st = sbase + s * SM::STAGE;
+    const int b = b0 + k;
+    constexpr uint32_t bytes =
+        (SM::SW * SM::SH + (LOAD_HIST ? 2 : 1) * SM::TILE) * (uint32_t)sizeof(T);
+    mbar_expect_tx(&bar[s], bytes);
+    // rows of a guarded plane: data row i lives at plane row kGuard + i
+    tma_load_3d(st, &a.f_halo[a.cur], &bar[s], j0 - kHalo, kGuard + i0 - kHalo, b);
+    tma_load_3d(st + SM::HALO, &a.s_tile, &bar[s], j0, kGuard + i0, b);
+    if (LOAD_HIST)
+      tma_load_3d(st + SM::HALO + SM::TILE, &a.h_tile, &bar[s], j0, i0,
+                  b * a.hist_steps + a.hist_slot);
+  };
+  if (tid == 0) issue(0);
 
   const int j = j0 + threadIdx.x;
-  if (j >= a.nxp) return;
-  const int jj = threadIdx.x + R;
-  const T pxj = a.px[j];
+  const bool vj = j < a.nxp;
+  const int rb = threadIdx.y * kNY;  // first tile row owned by this thread
+  const int ib = i0 + rb;
+  const int nq = vj ? max(0, min(kNY, a.nzp - ib)) : 0;
+  const int o0 = ib * a.ldx + j;     // offset of this thread's first cell
+  const int ldx = a.ldx;
+
+  // per-cell model data, reused for every shot of the group; the image
+  // accumulator starts from the stored image (prefetched, lands during shot 0)
+  T im[kNY], dd[kNY], img[kNY];
+  const T pxj = vj ? a.px[j] : T(0);
+  T* ig = nullptr;
+  if (LOAD_HIST) ig = a.image + (int64_t)grp * a.image_stride + o0;
 #pragma unroll
-  for (int q = 0; q < NY; ++q) {
-    const int ii = threadIdx.y + q * BY + R;
-    const int i = i0 + ii - R;
-    if (i >= a.nzp) break;
-    const T vc = s[ii][jj];
-    T lz = T(0), lx = T(0);
+  for (int q = 0; q < kNY; ++q) {
+    if (q < nq) {
+      im[q] = a.inv_m[o0 + q * ldx];
+      dd[q] = a.pz[ib + q] * pxj;
+      img[q] = LOAD_HIST ? ig[q * ldx] : T(0);
+    } else {
+      im[q] = T(0);
+      dd[q] = T(0);
+      img[q] = T(0);
+    }
+  }
+
+  for (int k = 0; k < nb; ++k) {
+    const int b = b0 + k;
+    if (tid == 0 && k + 1 < nb) issue(k + 1);
+
+    // does this tile hold a source tap of shot b?  (CTA-uniform)
+    bool src_here = false;
+    if (!ADJ && a.src_rc != nullptr) {
 #pragma unroll
-    for (int k = 1; k <= R; ++k) {
-      lz += a.cz[k] * ((s[ii - k][jj] - vc) + (s[ii + k][jj] - vc));
-      lx += a.cx[k] * ((s[ii][jj - k] - vc) + (s[ii][jj + k] - vc));
+      for (int t = 0; t < 4; ++t) {
+        const int r = a.src_rc[(b * 4 + t) * 2], c = a.src_rc[(b * 4 + t) * 2 + 1];
+        src_here |= (r >= i0 && r < i0 + kTH && c >= j0 && c < j0 + kBX);
+      }
     }
-    T lv = lz + lx;
-    const int o = i * a.ldx + j;
-    const int rr = i - a.inj_row0;
-    if (a.ybar != nullptr && rr >= 0 && rr < a.inj_nrows) {
-      // R^T y: duplicate taps accumulate (np.add.at, seisopt/wavesim.py:229)
-      const int cell = rr * a.nxp + j;
-      const int p1 = a.inj_ptr[cell + 1];
-      for (int p = a.inj_ptr[cell]; p < p1; ++p)
-        lv += a.inj_w[p] * a.ybar[(int64_t)b * a.ybar_stride + a.inj_rec[p]];
+    // receiver injection rows inside this tile?  (CTA-uniform)
+    const bool inj_here = ADJ && a.ybar != nullptr && a.inj_row0 < i0 + kTH &&
+                          a.inj_row0 + a.inj_nrows > i0;
+    const int64_t sb = (int64_t)b * a.plane;
+    T* __restrict__ fout = a.f[a.cur ^ 1] + sb + o0;
+    T* __restrict__ sout = a.state + sb + o0;
+    T* __restrict__ hout = nullptr;
+    if (!ADJ && HIST) hout = a.hist + ((int64_t)b * a.hist_steps + a.hist_slot) * a.hplane + o0;
+    const T* __restrict__ gin = nullptr;
+    if (GSRC) gin = a.gsrc + (int64_t)b * a.gsrc_stride + o0;
+
+    mbar_wait(&bar[k & 1], (k >> 1) & 1);
+    const T* st = sbase + (k & 1) * SM::STAGE;
+    // this thread's column, from tile row rb - R
+    const T* sc = st + (rb + HO) * SW + threadIdx.x + kHalo;
+    const T* sst = st + SM::HALO + rb * kBX + threadIdx.x;
+
+    if (nq > 0) {
+      T col[NCOL];
+#pragma unroll
+      for (int r = 0; r < NCOL; ++r) col[r] = sc[r * SW];
+#pragma unroll
+      for (int q = 0; q < kNY; ++q) {
+        if (q >= nq) break;
+        const T uc = col[q + R];
+        const T* row = sc + (q + R) * SW;
+        T lz = T(0), lx = T(0);
+#pragma unroll
+        for (int kk = 1; kk <= R; ++kk) {
+          lz += a.cz[kk] * ((col[q + R - kk] - uc) + (col[q + R + kk] - uc));
+          lx += a.cx[kk] * ((row[-kk] - uc) + (row[kk] - uc));
+        }
+        T lap = lz + lx;
+        const T sv = sst[q * kBX];
+        if (!ADJ) {
+          if (GSRC) lap += gin[q * ldx] * a.gscale[o0 + q * ldx];
+          T acc = lap * im[q];
+          if (src_here) {
+            const int i = ib + q;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int r = a.src_rc[(b * 4 + t) * 2], c = a.src_rc[(b * 4 + t) * 2 + 1];
+              if (r == i && c == j) acc += a.amp * a.src_w[b * 4 + t] * im[q];
+            }
+          }
+          if (HIST) hout[q * ldx] = acc;
+          const T so = dd[q] * (sv + a.dt2 * acc);
+          sout[q * ldx] = so;
+          fout[q * ldx] = dd[q] * uc + so;
+        } else {
+          if (inj_here) {
+            const int rr = ib + q - a.inj_row0;
+            if (rr >= 0 && rr < a.inj_nrows) {
+              // R^T y: duplicate taps accumulate (np.add.at, seisopt/wavesim.py:229)
+              const int cell = rr * a.nxp + j;
+              const int p1 = a.inj_ptr[cell + 1];
+              for (int p = a.inj_ptr[cell]; p < p1; ++p)
+                lap += a.inj_w[p] * a.ybar[(int64_t)b * a.ybar_stride + a.inj_rec[p]];
+            }
+          }
+          const T so = dd[q] * sv + lap;
+          sout[q * ldx] = so;
+          fout[q * ldx] = dd[q] * uc + (a.dt2 * im[q] * dd[q]) * so;
+          if (LOAD_HIST) img[q] -= sst[q * kBX + SM::TILE] * uc;
+          if (VHIST) a.vhist[(int64_t)b * a.vhist_stride + o0 + q * ldx] = uc;
+        }
+      }
     }
-    const T d = a.pz[i] * pxj;
-    const int64_t fo = (int64_t)b * a.plane + o;
-    const T wn = d * a.w[fo] + lv;
-    a.w[fo] = wn;
-    a.lam_next[fo] = d * lam[o] + wn;
-    if (a.image != nullptr)
-      a.image[(int64_t)b * a.image_stride + o] -= a.hist[(int64_t)b * a.hist_stride + o] * vc;
-    if (a.vhist != nullptr) a.vhist[(int64_t)b * a.vhist_stride + o] = vc;
+    __syncthreads();  // stage (k & 1) is free for shot k + 2
+  }
+  if (LOAD_HIST) {
+#pragma unroll
+    for (int q = 0; q < kNY; ++q)
+      if (q < nq) ig[q * ldx] = img[q];
   }
 }
 

@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -33,9 +34,27 @@ using namespace sg;
 
 namespace {
 
-constexpr int BX = 64, BY = 4, NY = 8, TH = BY * NY;  // 64 x 32 tiles, 256 threads
-constexpr int RB = BX * BY;                           // receiver threads per block
-constexpr int kSlack = 256;                           // column slack for profile arrays
+constexpr int BX = kBX, TH = kTH;  // 64 x 32 tiles, 256 threads
+constexpr int RB = kBX * kBY;       // threads per block
+constexpr int kSlack = 256;         // column slack for profile arrays
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
 
 // ---------------------------------------------------------------------------
 // small kernels
@@ -203,7 +222,7 @@ struct sg_handle {
   void* pz_buf = nullptr;
   void* px_buf = nullptr;
   void* gscale_buf = nullptr;  // -m_r on the padded grid (Born)
-  int* src_ij = nullptr;
+  int* src_rc = nullptr;  // (n_shots, 4, 2) tap rows/cols
   void* src_w = nullptr;
   int* rec_ij = nullptr;
   void* rec_w = nullptr;
@@ -220,8 +239,10 @@ struct sg_handle {
   int recon = SG_RECON_FULL;
   int K = 0, ncp = 0;     // checkpoint interval / count
   int64_t hist_steps = 0; // steps of history held per shot
-  int* bsrc_ij = nullptr;
+  int G = 1;              // shots per CTA group
+  int* bsrc_rc = nullptr;
   void* bsrc_w = nullptr;
+  std::map<std::string, CUtensorMap> tmaps;  // TMA descriptors by buffer/kind
   void *u0 = nullptr, *u1 = nullptr, *inc = nullptr;
   void *l0 = nullptr, *l1 = nullptr, *w = nullptr;
   void* gath = nullptr;
@@ -280,7 +301,8 @@ void drop_graphs(sg_handle* h) {
 
 void free_batch(sg_handle* h) {
   drop_graphs(h);
-  void** bufs[] = {(void**)&h->bsrc_ij, &h->bsrc_w, &h->u0, &h->u1, &h->inc, &h->l0, &h->l1,
+  h->tmaps.clear();
+  void** bufs[] = {(void**)&h->bsrc_rc, &h->bsrc_w, &h->u0, &h->u1, &h->inc, &h->l0, &h->l1,
                    &h->w, &h->gath, &h->hist, &h->ckpt, &h->img, &h->acc_img,
                    (void**)&h->part, (void**)&h->scal};
   for (auto p : bufs) dfree(p);
@@ -318,13 +340,22 @@ int ensure_batch(sg_handle* h) {
     return fail(SG_ERR_OOM, "one shot needs " + std::to_string(per / 1e9) +
                                 " GB of device memory; budget " + std::to_string(budget / 1e9));
   h->B = B;
+  // shots per CTA group: model data and the image accumulator are amortised
+  // over G shots; keep >= ~3 CTAs per SM
+  int G = h->d.group;
+  if (G <= 0) {
+    const char* e = getenv("SG_GROUP");
+    G = e ? atoi(e) : 0;
+  }
+  if (G <= 0) G = (int)std::floor((double)B * h->ntiles / (148.0 * 3.0));
+  h->G = std::max(1, std::min({G, 8, B}));
   h->recon = recon;
   h->K = K;
   h->ncp = ncp;
   h->hist_steps = recon == SG_RECON_FULL ? nt : K;
   const size_t e = h->esz;
   const size_t fb = ((size_t)h->ldx + (size_t)B * h->plane + h->tail) * e;
-  SG_TRY(dalloc(h, (void**)&h->bsrc_ij, (size_t)B * 4 * sizeof(int)));
+  SG_TRY(dalloc(h, (void**)&h->bsrc_rc, (size_t)B * 8 * sizeof(int)));
   SG_TRY(dalloc(h, &h->bsrc_w, (size_t)B * 4 * e));
   SG_TRY(dalloc(h, &h->u0, fb));
   SG_TRY(dalloc(h, &h->u1, fb));
@@ -348,9 +379,66 @@ int ensure_batch(sg_handle* h) {
 // kernel argument builders + launchers
 // ---------------------------------------------------------------------------
 
+int ngroups(const sg_handle* h, int count) { return (count + h->G - 1) / h->G; }
+
+// TMA descriptors.  Guarded buffers (fields, state) are viewed as 3-D
+// {ldx, nzp + 2 kGuard, B} starting after the lead row; histories as
+// {ldx, nzp, planes}.  Out-of-bounds boxes read as zero and are clipped on store.
+enum MapKind { MAP_HALO = 0, MAP_TILE = 1, MAP_HIST = 2 };
+
+template <typename T, int R>
+int get_map(sg_handle* h, void* base, int kind, int64_t planes, CUtensorMap* out) {
+  char keyb[96];
+  snprintf(keyb, sizeof keyb, "%p/%d/%lld/%d", base, kind, (long long)planes, R);
+  const std::string key(keyb);
+  auto it = h->tmaps.find(key);
+  if (it != h->tmaps.end()) {
+    *out = it->second;
+    return SG_OK;
+  }
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(SG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int rows = (kind == MAP_HIST) ? h->nzp : h->nzp + 2 * kGuard;
+  const int64_t pl = (kind == MAP_HIST) ? h->hplane : h->plane;
+  void* g = (kind == MAP_HIST) ? base : (void*)((char*)base + (size_t)h->ldx * sizeof(T));
+  cuuint64_t dims[3] = {(cuuint64_t)h->ldx, (cuuint64_t)rows, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)h->ldx * sizeof(T), (cuuint64_t)pl * sizeof(T)};
+  cuuint32_t box[3] = {(cuuint32_t)(kind == MAP_HALO ? BX + 2 * kHalo : BX),
+                       (cuuint32_t)(kind == MAP_HALO ? TH + 2 * kHalo : TH), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMap m;
+  CUresult r = enc(&m, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                   3, g, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(SG_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  h->tmaps[key] = m;
+  *out = m;
+  return SG_OK;
+}
+
+template <typename T, int R>
+int step_maps(sg_handle* h, StepArgs<T>& a, void* F0, void* F1, void* state, void* hist,
+              int64_t hist_planes) {
+  SG_TRY((get_map<T, R>(h, F0, MAP_HALO, h->B, &a.f_halo[0])));
+  SG_TRY((get_map<T, R>(h, F1, MAP_HALO, h->B, &a.f_halo[1])));
+  SG_TRY((get_map<T, R>(h, F0, MAP_TILE, h->B, &a.f_tile[0])));
+  SG_TRY((get_map<T, R>(h, F1, MAP_TILE, h->B, &a.f_tile[1])));
+  SG_TRY((get_map<T, R>(h, state, MAP_TILE, h->B, &a.s_tile)));
+  if (hist) SG_TRY((get_map<T, R>(h, hist, MAP_HIST, hist_planes, &a.h_tile)));
+  return SG_OK;
+}
+
 template <typename T>
-FwdArgs<T> fwd_args(const sg_handle* h) {
-  FwdArgs<T> a{};
+int step_args(sg_handle* h, StepArgs<T>& a, void* F0, void* F1, void* state, void* hist,
+              int64_t hist_planes) {
+  std::memset(&a, 0, sizeof(a));
+  if (h->d.order == 8) SG_TRY((step_maps<T, 4>(h, a, F0, F1, state, hist, hist_planes)));
+  else SG_TRY((step_maps<T, 1>(h, a, F0, F1, state, hist, hist_planes)));
+  a.f[0] = field<T>(F0, h);
+  a.f[1] = field<T>(F1, h);
+  a.state = field<T>(state, h);
   a.inv_m = field<T>(h->inv_m_buf, h);
   a.pz = reinterpret_cast<const T*>(h->pz_buf) + kGuard;
   a.px = reinterpret_cast<const T*>(h->px_buf) + kGuard;
@@ -360,6 +448,7 @@ FwdArgs<T> fwd_args(const sg_handle* h) {
   a.ldx = h->ldx;
   a.tiles_x = h->tiles_x;
   a.ntiles = h->ntiles;
+  a.G = h->G;
   a.dt2 = (T)(h->d.dt * h->d.dt);
   for (int k = 0; k < 5; ++k) {
     a.cz[k] = (T)h->cz[k];
@@ -368,65 +457,87 @@ FwdArgs<T> fwd_args(const sg_handle* h) {
   a.rec_ij = h->rec_ij;
   a.rec_w = reinterpret_cast<const T*>(h->rec_w);
   a.nrec = h->d.n_rec;
-  return a;
-}
-
-template <typename T>
-AdjArgs<T> adj_args(const sg_handle* h) {
-  AdjArgs<T> a{};
-  a.inv_m = field<T>(h->inv_m_buf, h);
-  a.pz = reinterpret_cast<const T*>(h->pz_buf) + kGuard;
-  a.px = reinterpret_cast<const T*>(h->px_buf) + kGuard;
-  a.plane = h->plane;
-  a.nzp = h->nzp;
-  a.nxp = h->nxp;
-  a.ldx = h->ldx;
-  a.tiles_x = h->tiles_x;
-  a.ntiles = h->ntiles;
-  a.dt2 = (T)(h->d.dt * h->d.dt);
-  for (int k = 0; k < 5; ++k) {
-    a.cz[k] = (T)h->cz[k];
-    a.cx[k] = (T)h->cx[k];
-  }
+  a.rec_blocks = (h->G * h->d.n_rec + RB - 1) / RB;
   a.inj_row0 = h->inj_row0;
   a.inj_nrows = h->inj_nrows;
   a.inj_ptr = h->inj_ptr;
   a.inj_rec = h->inj_rec;
   a.inj_w = reinterpret_cast<const T*>(h->inj_w);
-  return a;
+  return SG_OK;
 }
 
-template <typename T>
-void launch_fwd(const sg_handle* h, cudaStream_t s, const FwdArgs<T>& a, int count) {
-  dim3 grid(h->ntiles + (a.gather ? h->rec_blocks : 0), count), block(BX, BY);
-  if (h->d.order == 8) k_forward_step<T, 4, BX, BY, NY><<<grid, block, 0, s>>>(a);
-  else k_forward_step<T, 1, BX, BY, NY><<<grid, block, 0, s>>>(a);
+template <typename T, int R, bool ADJ, int FL>
+void launch_step_f(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a) {
+  static bool attr = false;
+  constexpr int smem = step_smem_bytes<T, R, ADJ>();
+  if (!attr) {
+    cudaFuncSetAttribute(k_step<T, R, ADJ, FL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
+    attr = true;
+  }
+  const int extra = (!ADJ && (FL & FL_GATHER)) ? a.rec_blocks : 0;
+  dim3 grid(h->ntiles + extra, ngroups(h, a.count)), block(kBX, kBY);
+  k_step<T, R, ADJ, FL><<<grid, block, smem, s>>>(a);
   count_launch();
 }
 
-template <typename T>
-void launch_adj(const sg_handle* h, cudaStream_t s, const AdjArgs<T>& a, int count) {
-  dim3 grid(h->ntiles, count), block(BX, BY);
-  if (h->d.order == 8) k_adjoint_step<T, 4, BX, BY, NY><<<grid, block, 0, s>>>(a);
-  else k_adjoint_step<T, 1, BX, BY, NY><<<grid, block, 0, s>>>(a);
-  count_launch();
+template <typename T, int R, bool ADJ>
+void launch_step_r(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a) {
+  const int fl = (a.hist_on ? FL_HIST : 0) | (a.gsrc ? FL_GSRC : 0) |
+                 (a.vhist ? FL_VHIST : 0) | (a.gather ? FL_GATHER : 0);
+  if (ADJ) {
+    if (fl & FL_VHIST) launch_step_f<T, R, ADJ, FL_VHIST>(h, s, a);
+    else if (fl & FL_HIST) launch_step_f<T, R, ADJ, FL_HIST>(h, s, a);
+    else launch_step_f<T, R, ADJ, 0>(h, s, a);
+    return;
+  }
+  switch (fl & (FL_HIST | FL_GSRC | FL_GATHER)) {
+    case 0: launch_step_f<T, R, ADJ, 0>(h, s, a); break;
+    case FL_HIST: launch_step_f<T, R, ADJ, FL_HIST>(h, s, a); break;
+    case FL_GATHER: launch_step_f<T, R, ADJ, FL_GATHER>(h, s, a); break;
+    case FL_HIST | FL_GATHER: launch_step_f<T, R, ADJ, FL_HIST | FL_GATHER>(h, s, a); break;
+    case FL_GSRC: launch_step_f<T, R, ADJ, FL_GSRC>(h, s, a); break;
+    case FL_GSRC | FL_GATHER: launch_step_f<T, R, ADJ, FL_GSRC | FL_GATHER>(h, s, a); break;
+    case FL_GSRC | FL_HIST: launch_step_f<T, R, ADJ, FL_GSRC | FL_HIST>(h, s, a); break;
+    default: launch_step_f<T, R, ADJ, FL_GSRC | FL_HIST | FL_GATHER>(h, s, a); break;
+  }
+}
+
+template <typename T, bool ADJ>
+void launch_step(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a) {
+  if (h->d.order == 8) launch_step_r<T, 4, ADJ>(h, s, a);
+  else launch_step_r<T, 1, ADJ>(h, s, a);
 }
 
 // ---- sweep pieces (enqueue only) --------------------------------------------
 
+// A history buffer holds `steps` planes per shot for `shots` shots:
+// plane index = b * steps + slot.
+struct HistRef {
+  void* base = nullptr;
+  int steps = 0;
+  int64_t shots = 0;
+  int n0 = 0;           // step stored at slot 0
+  bool rotate = false;  // slot = (n - n0) % steps
+  int slot(int n) const { return rotate ? (n - n0) % steps : n - n0; }
+};
+
+HistRef main_hist(const sg_handle* h, int n0) {
+  HistRef r;
+  r.base = h->hist;
+  r.steps = (int)h->hist_steps;
+  r.shots = h->B;
+  r.n0 = n0;
+  return r;
+}
+
 struct FwdPlan {
   bool point = true;        // wavelet point source
   bool gathers = true;      // sample receivers into h->gath
-  void* hist = nullptr;     // history base (per-shot stride hist_shot, step stride hplane)
-  int64_t hist_shot = 0;
-  int hist_n0 = 0;          // step index stored at slot 0
-  bool hist_mod = false;    // slot = (n - hist_n0) % hist_len (rotating)
-  int hist_len = 0;
-  const void* gsrc = nullptr;  // Born source history (same addressing as hist)
+  HistRef hist;             // acceleration store
+  const void* gsrc = nullptr;  // Born source history (per shot gsrc_shot elements)
   int64_t gsrc_shot = 0;
   int gsrc_n0 = 0;
-  bool gsrc_mod = false;
-  int gsrc_len = 0;
   bool ckpt_save = false;   // save (u_n, inc_n) at n % K == 0
   void* fu0 = nullptr;      // field buffers (default u0/u1/inc)
   void* fu1 = nullptr;
@@ -434,80 +545,71 @@ struct FwdPlan {
 };
 
 template <typename T>
-void enq_forward(sg_handle* h, cudaStream_t s, int count, int n0, int n1, const FwdPlan& p) {
+int enq_forward(sg_handle* h, cudaStream_t s, int count, int n0, int n1, const FwdPlan& p) {
   void* U0 = p.fu0 ? p.fu0 : h->u0;
   void* U1 = p.fu1 ? p.fu1 : h->u1;
   void* INC = p.finc ? p.finc : h->inc;
-  FwdArgs<T> a = fwd_args<T>(h);
-  a.inc = field<T>(INC, h);
+  StepArgs<T> a;
+  SG_TRY(step_args<T>(h, a, U0, U1, INC, p.hist.base, p.hist.shots * p.hist.steps));
+  a.count = count;
   if (p.point) {
-    a.src_ij = h->bsrc_ij;
+    a.src_rc = h->bsrc_rc;
     a.src_w = reinterpret_cast<const T*>(h->bsrc_w);
   }
   if (p.gsrc) {
     a.gscale = field<T>(h->gscale_buf, h);
     a.gsrc_stride = p.gsrc_shot;
   }
-  a.hist_stride = p.hist_shot;
+  a.hist_on = p.hist.base != nullptr;
+  a.hist_steps = p.hist.steps;
+  a.hist = reinterpret_cast<T*>(p.hist.base);
+  a.hplane = h->hplane;
   a.gather_stride = (int64_t)h->d.nt * h->d.n_rec;
   const size_t pb = span_bytes(h, count);
   const size_t sb = span_bytes(h, h->B);
   for (int n = n0; n < n1; ++n) {
-    const bool odd = ((n - n0) & 1) != 0;
-    void* cur = odd ? U1 : U0;
-    void* nxt = odd ? U0 : U1;
+    a.cur = (n - n0) & 1;
     if (p.ckpt_save && n % h->K == 0) {
       char* slot = (char*)h->ckpt + (size_t)(n / h->K) * 2 * sb;
-      cudaMemcpyAsync(slot, cur, pb, cudaMemcpyDeviceToDevice, s);
+      cudaMemcpyAsync(slot, a.cur ? U1 : U0, pb, cudaMemcpyDeviceToDevice, s);
       cudaMemcpyAsync(slot + sb, INC, pb, cudaMemcpyDeviceToDevice, s);
     }
-    a.u = field<T>(cur, h);
-    a.u_next = field<T>(nxt, h);
     a.amp = (T)h->wavelet[n];
-    if (p.hist) {
-      const int slot = p.hist_mod ? (n - p.hist_n0) % p.hist_len : (n - p.hist_n0);
-      a.hist = reinterpret_cast<T*>(p.hist) + (int64_t)slot * h->hplane;
-    } else {
-      a.hist = nullptr;
-    }
-    if (p.gsrc) {
-      const int slot = p.gsrc_mod ? (n - p.gsrc_n0) % p.gsrc_len : (n - p.gsrc_n0);
-      a.gsrc = reinterpret_cast<const T*>(p.gsrc) + (int64_t)slot * h->hplane;
-    }
+    if (a.hist_on) a.hist_slot = p.hist.slot(n);
+    if (p.gsrc) a.gsrc = reinterpret_cast<const T*>(p.gsrc) + (int64_t)(n - p.gsrc_n0) * h->hplane;
     a.gather = p.gathers ? reinterpret_cast<T*>(h->gath) + (int64_t)n * h->d.n_rec : nullptr;
-    launch_fwd<T>(h, s, a, count);
+    launch_step<T, false>(h, s, a);
   }
+  return SG_OK;
 }
 
 struct AdjPlan {
-  const void* hist = nullptr;  // imaging history (nullptr: no imaging)
-  int64_t hist_shot = 0;
-  int hist_n0 = 0;
+  HistRef hist;                // imaging history (base nullptr: no imaging)
   bool inject = true;          // y from h->gath (scaled residual / data)
-  void* vhist = nullptr;       // optional v store
-  int64_t vhist_shot = 0;
+  void* vhist = nullptr;       // optional v store (nt planes, compact rows)
 };
 
+// adjoint steps n = n_hi-1 .. n_lo; state V in l0/l1 (parity from n), w in place
 template <typename T>
-void enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, const AdjPlan& p) {
-  AdjArgs<T> a = adj_args<T>(h);
-  a.w = field<T>(h->w, h);
+int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, const AdjPlan& p) {
+  StepArgs<T> a;
+  SG_TRY(step_args<T>(h, a, h->l0, h->l1, h->w, p.hist.base, p.hist.shots * p.hist.steps));
+  a.count = count;
   a.ybar_stride = (int64_t)h->d.nt * h->d.n_rec;
-  a.hist_stride = p.hist_shot;
-  a.image = p.hist ? reinterpret_cast<T*>(h->img) : nullptr;
+  a.hist_on = p.hist.base != nullptr;
+  a.hist_steps = p.hist.steps;
+  a.image = a.hist_on ? reinterpret_cast<T*>(h->img) : nullptr;
   a.image_stride = h->hplane;
-  a.vhist_stride = p.vhist_shot;
+  a.vhist_stride = (int64_t)h->d.nt * h->hplane;
   const int nt = h->d.nt;
   for (int n = n_hi - 1; n >= n_lo; --n) {
-    const bool odd = ((nt - 1 - n) & 1) != 0;
-    a.lam = field<T>(odd ? h->l1 : h->l0, h);
-    a.lam_next = field<T>(odd ? h->l0 : h->l1, h);
+    a.cur = (nt - 1 - n) & 1;
     a.ybar = p.inject ? reinterpret_cast<const T*>(h->gath) + (int64_t)n * h->d.n_rec : nullptr;
-    a.hist = p.hist ? reinterpret_cast<const T*>(p.hist) + (int64_t)(n - p.hist_n0) * h->hplane
-                    : nullptr;
+    if (a.hist_on) a.hist_slot = p.hist.slot(n);
     a.vhist = p.vhist ? reinterpret_cast<T*>(p.vhist) + (int64_t)n * h->hplane : nullptr;
-    launch_adj<T>(h, s, a, count);
+    launch_step<T, true>(h, s, a);
   }
+  return SG_OK;
 }
 
 // ---- graph capture / replay ---------------------------------------------------
@@ -515,7 +617,7 @@ void enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, co
 template <typename F>
 int run_graph(sg_handle* h, const std::string& key, F&& body) {
   if (!h->d.use_graphs) {
-    body(h->stream);
+    SG_TRY(body(h->stream));
     SG_CK(cudaGetLastError());
     return SG_OK;
   }
@@ -524,9 +626,13 @@ int run_graph(sg_handle* h, const std::string& key, F&& body) {
     if (!h->cap) SG_CK(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
     const int64_t before = g_launches.load();
     SG_CK(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
-    body(h->cap);
+    const int brc = body(h->cap);
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(h->cap, &g);
+    if (brc != SG_OK) {
+      if (g) cudaGraphDestroy(g);
+      return brc;
+    }
     if (e != cudaSuccess)
       return fail(SG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
     const int64_t nk = g_launches.load() - before;  // kernels per replay
@@ -573,7 +679,7 @@ int check_range(sg_handle* h, int shot0, int count) {
 
 // load batch-local source taps for shots [b0, b0+cnt)
 int load_batch_sources(sg_handle* h, int b0, int cnt) {
-  SG_CK(cudaMemcpyAsync(h->bsrc_ij, h->src_ij + (size_t)b0 * 4, (size_t)cnt * 4 * sizeof(int),
+  SG_CK(cudaMemcpyAsync(h->bsrc_rc, h->src_rc + (size_t)b0 * 8, (size_t)cnt * 8 * sizeof(int),
                         cudaMemcpyDeviceToDevice, h->stream));
   SG_CK(cudaMemcpyAsync(h->bsrc_w, (char*)h->src_w + (size_t)b0 * 4 * h->esz,
                         (size_t)cnt * 4 * h->esz, cudaMemcpyDeviceToDevice, h->stream));
@@ -613,7 +719,7 @@ template <typename T>
 int reduce_images(sg_handle* h, int cnt) {
   dim3 grid(cdiv(h->nxp, 128), h->nzp);
   k_reduce_images<T><<<grid, 128, 0, h->stream>>>(
-      reinterpret_cast<const T*>(h->img), reinterpret_cast<T*>(h->acc_img), cnt, h->hplane,
+      reinterpret_cast<const T*>(h->img), reinterpret_cast<T*>(h->acc_img), ngroups(h, cnt), h->hplane,
       h->nzp, h->nxp, h->ldx);
   count_launch();
   SG_CK(cudaGetLastError());
@@ -644,24 +750,26 @@ int do_forward_batch(sg_handle* h, int b0, int cnt, bool store_full_hist_ckpt_mo
   SG_TRY(zero_fields(h, true, false, cnt));
   const int nt = h->d.nt;
   if (!store_full_hist_ckpt_mode) {
-    SG_TRY(run_graph(h, "fwd_plain/" + std::to_string(cnt), [&](cudaStream_t s) {
+    SG_TRY(run_graph(h, "fwd_plain/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
       FwdPlan p;
-      enq_forward<T>(h, s, cnt, 0, nt, p);
+      SG_TRY(enq_forward<T>(h, s, cnt, 0, nt, p));
+      return SG_OK;
     }));
     return SG_OK;
   }
   if (h->recon == SG_RECON_FULL) {
-    SG_TRY(run_graph(h, "fwd_full/" + std::to_string(cnt), [&](cudaStream_t s) {
+    SG_TRY(run_graph(h, "fwd_full/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
       FwdPlan p;
-      p.hist = h->hist;
-      p.hist_shot = (int64_t)h->hist_steps * h->hplane;
-      enq_forward<T>(h, s, cnt, 0, nt, p);
+      p.hist = main_hist(h, 0);
+      SG_TRY(enq_forward<T>(h, s, cnt, 0, nt, p));
+      return SG_OK;
     }));
   } else {
-    SG_TRY(run_graph(h, "fwd_ckpt/" + std::to_string(cnt), [&](cudaStream_t s) {
+    SG_TRY(run_graph(h, "fwd_ckpt/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
       FwdPlan p;
       p.ckpt_save = true;
-      enq_forward<T>(h, s, cnt, 0, nt, p);
+      SG_TRY(enq_forward<T>(h, s, cnt, 0, nt, p));
+      return SG_OK;
     }));
   }
   return SG_OK;
@@ -670,25 +778,30 @@ int do_forward_batch(sg_handle* h, int b0, int cnt, bool store_full_hist_ckpt_mo
 // adjoint over all steps with imaging against the forward history of the
 // current batch (FULL: stored; CHECKPOINT: segment recompute from checkpoints)
 template <typename T>
-int do_adjoint_batch(sg_handle* h, int cnt, const void* cached_hist, int64_t cached_shot) {
+int do_adjoint_batch(sg_handle* h, int cnt, const void* cached_hist, int64_t cached_shots) {
   SG_TRY(zero_fields(h, false, true, cnt));
   SG_CK(cudaMemsetAsync(h->img, 0, (size_t)cnt * h->hplane * h->esz, h->stream));
   const int nt = h->d.nt;
   if (cached_hist != nullptr || h->recon == SG_RECON_FULL) {
-    const void* hb = cached_hist ? cached_hist : h->hist;
-    const int64_t hs = cached_hist ? cached_shot : (int64_t)h->hist_steps * h->hplane;
+    HistRef hr = main_hist(h, 0);
+    if (cached_hist) {
+      hr.base = const_cast<void*>(cached_hist);
+      hr.steps = nt;
+      hr.shots = cached_shots;
+    }
+    const void* hb = hr.base;
     std::string key = std::string(cached_hist ? "adj_cached/" : "adj_full/") +
                       std::to_string(cnt) + "/" + std::to_string((uintptr_t)hb);
-    SG_TRY(run_graph(h, key, [&](cudaStream_t s) {
+    SG_TRY(run_graph(h, key, [&](cudaStream_t s) -> int {
       AdjPlan p;
-      p.hist = hb;
-      p.hist_shot = hs;
-      enq_adjoint<T>(h, s, cnt, nt, 0, p);
+      p.hist = hr;
+      SG_TRY(enq_adjoint<T>(h, s, cnt, nt, 0, p));
+      return SG_OK;
     }));
     return SG_OK;
   }
   // CHECKPOINT: per segment restore -> forward with segment history -> adjoint
-  SG_TRY(run_graph(h, "adj_ckpt/" + std::to_string(cnt), [&](cudaStream_t s) {
+  SG_TRY(run_graph(h, "adj_ckpt/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
     const size_t pb = span_bytes(h, cnt);
     const size_t sb = span_bytes(h, h->B);
     for (int seg = h->ncp - 1; seg >= 0; --seg) {
@@ -699,16 +812,13 @@ int do_adjoint_batch(sg_handle* h, int cnt, const void* cached_hist, int64_t cac
       cudaMemcpyAsync(h->inc, slot + sb, pb, cudaMemcpyDeviceToDevice, s);
       FwdPlan fp;
       fp.gathers = false;
-      fp.hist = h->hist;
-      fp.hist_shot = (int64_t)h->hist_steps * h->hplane;
-      fp.hist_n0 = n0;
-      enq_forward<T>(h, s, cnt, n0, n1, fp);
+      fp.hist = main_hist(h, n0);
+      SG_TRY(enq_forward<T>(h, s, cnt, n0, n1, fp));
       AdjPlan ap;
-      ap.hist = h->hist;
-      ap.hist_shot = (int64_t)h->hist_steps * h->hplane;
-      ap.hist_n0 = n0;
-      enq_adjoint<T>(h, s, cnt, n1, n0, ap);
+      ap.hist = main_hist(h, n0);
+      SG_TRY(enq_adjoint<T>(h, s, cnt, n1, n0, ap));
     }
+    return SG_OK;
   }));
   return SG_OK;
 }
@@ -819,12 +929,14 @@ int born_cache_t(sg_handle* h, int shot0, int count) {
     SG_TRY(zero_fields(h, true, false, cnt));
     void* base = (char*)h->born_hist + (size_t)(b0 - shot0) * per;
     SG_TRY(run_graph(h, "born_fill/" + std::to_string(cnt) + "/" + std::to_string((uintptr_t)base),
-                     [&](cudaStream_t s) {
+                     [&](cudaStream_t s) -> int {
                        FwdPlan p;
                        p.gathers = false;
-                       p.hist = base;
-                       p.hist_shot = (int64_t)nt * h->hplane;
-                       enq_forward<T>(h, s, cnt, 0, nt, p);
+                       p.hist.base = base;
+                       p.hist.steps = nt;
+                       p.hist.shots = count - (b0 - shot0);
+                       SG_TRY(enq_forward<T>(h, s, cnt, 0, nt, p));
+                       return SG_OK;
                      }));
   }
   SG_CK(cudaStreamSynchronize(h->stream));
@@ -845,29 +957,28 @@ int born_forward_t(sg_handle* h, int shot0, int count, const void* m_r, void* ou
       const void* base = (char*)h->born_hist + (size_t)(b0 - h->born_b0) * nt * h->hplane * h->esz;
       SG_TRY(run_graph(h, "born_fwd_cached/" + std::to_string(cnt) + "/" +
                               std::to_string((uintptr_t)base),
-                       [&](cudaStream_t s) {
+                       [&](cudaStream_t s) -> int {
                          FwdPlan p;
                          p.point = false;
                          p.gsrc = base;
                          p.gsrc_shot = (int64_t)nt * h->hplane;
-                         enq_forward<T>(h, s, cnt, 0, nt, p);
+                         SG_TRY(enq_forward<T>(h, s, cnt, 0, nt, p));
+                         return SG_OK;
                        }));
     } else {
       // lock-step: background step writes a0_n into a one-slot buffer, the
       // scattered step (fields l0/l1/w) consumes it in the same stream order
       SG_TRY(load_batch_sources(h, b0, cnt));
       SG_TRY(zero_fields(h, true, true, cnt));
-      SG_TRY(run_graph(h, "born_fwd_lock/" + std::to_string(cnt), [&](cudaStream_t s) {
+      SG_TRY(run_graph(h, "born_fwd_lock/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
         for (int n = 0; n < nt; ++n) {
           FwdPlan bg;
           bg.gathers = false;
-          bg.hist = h->hist;
-          bg.hist_shot = (int64_t)h->hist_steps * h->hplane;
-          bg.hist_n0 = n;
+          bg.hist = main_hist(h, n);
           // alternate the background ping-pong by running one step at a time
           bg.fu0 = (n & 1) ? h->u1 : h->u0;
           bg.fu1 = (n & 1) ? h->u0 : h->u1;
-          enq_forward<T>(h, s, cnt, n, n + 1, bg);
+          SG_TRY(enq_forward<T>(h, s, cnt, n, n + 1, bg));
           FwdPlan sc;
           sc.point = false;
           sc.gsrc = h->hist;
@@ -876,8 +987,9 @@ int born_forward_t(sg_handle* h, int shot0, int count, const void* m_r, void* ou
           sc.fu0 = (n & 1) ? h->l1 : h->l0;
           sc.fu1 = (n & 1) ? h->l0 : h->l1;
           sc.finc = h->w;
-          enq_forward<T>(h, s, cnt, n, n + 1, sc);
+          SG_TRY(enq_forward<T>(h, s, cnt, n, n + 1, sc));
         }
+        return SG_OK;
       }));
     }
     SG_TRY(copy_gathers_out<T>(h, (char*)out + (size_t)(b0 - shot0) * gper, cnt));
@@ -907,27 +1019,28 @@ int born_adjoint_core(sg_handle* h, int shot0, int count, const void* data, int 
     }
     if (born_cached_covers(h, b0, cnt)) {
       const void* base = (char*)h->born_hist + (size_t)(b0 - h->born_b0) * nt * h->hplane * h->esz;
-      SG_TRY(do_adjoint_batch<T>(h, cnt, base, (int64_t)nt * h->hplane));
+      SG_TRY(do_adjoint_batch<T>(h, cnt, base, h->born_count - (b0 - h->born_b0)));
     } else if (h->recon == SG_RECON_FULL) {
       // recompute and store the background history, then image against it
       SG_TRY(load_batch_sources(h, b0, cnt));
       SG_TRY(zero_fields(h, true, false, cnt));
-      SG_TRY(run_graph(h, "born_bg_full/" + std::to_string(cnt), [&](cudaStream_t s) {
+      SG_TRY(run_graph(h, "born_bg_full/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
         FwdPlan p;
         p.gathers = false;
-        p.hist = h->hist;
-        p.hist_shot = (int64_t)h->hist_steps * h->hplane;
-        enq_forward<T>(h, s, cnt, 0, nt, p);
+        p.hist = main_hist(h, 0);
+        SG_TRY(enq_forward<T>(h, s, cnt, 0, nt, p));
+        return SG_OK;
       }));
       SG_TRY(do_adjoint_batch<T>(h, cnt, nullptr, 0));
     } else {
       SG_TRY(load_batch_sources(h, b0, cnt));
       SG_TRY(zero_fields(h, true, false, cnt));
-      SG_TRY(run_graph(h, "born_bg_ckpt/" + std::to_string(cnt), [&](cudaStream_t s) {
+      SG_TRY(run_graph(h, "born_bg_ckpt/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
         FwdPlan p;
         p.gathers = false;
         p.ckpt_save = true;
-        enq_forward<T>(h, s, cnt, 0, nt, p);
+        SG_TRY(enq_forward<T>(h, s, cnt, 0, nt, p));
+        return SG_OK;
       }));
       SG_TRY(do_adjoint_batch<T>(h, cnt, nullptr, 0));
     }
@@ -953,9 +1066,10 @@ int forward_history_t(sg_handle* h, int shot, void* gather, void* accel) {
   SG_TRY(load_batch_sources(h, shot, 1));
   SG_TRY(zero_fields(h, true, false, 1));
   FwdPlan p;
-  p.hist = tmp;
-  p.hist_shot = (int64_t)nt * h->hplane;
-  enq_forward<T>(h, h->stream, 1, 0, nt, p);
+  p.hist.base = tmp;
+  p.hist.steps = nt;
+  p.hist.shots = 1;
+  SG_TRY(enq_forward<T>(h, h->stream, 1, 0, nt, p));
   SG_CK(cudaGetLastError());
   SG_TRY(copy_gathers_out<T>(h, gather, 1));
   dim3 grid(cdiv(h->nxp, 128), 4096);
@@ -978,8 +1092,7 @@ int adjoint_history_t(sg_handle* h, const void* ybar, void* vout) {
   SG_TRY(zero_fields(h, false, true, 1));
   AdjPlan p;
   p.vhist = tmp;
-  p.vhist_shot = (int64_t)nt * h->hplane;
-  enq_adjoint<T>(h, h->stream, 1, nt, 0, p);
+  SG_TRY(enq_adjoint<T>(h, h->stream, 1, nt, 0, p));
   SG_CK(cudaGetLastError());
   dim3 grid(cdiv(h->nxp, 128), 4096);
   k_unpitch<T><<<grid, 128, 0, h->stream>>>(reinterpret_cast<T*>(tmp), reinterpret_cast<T*>(vout),
@@ -1002,28 +1115,24 @@ int time_kernel_t(sg_handle* h, int which, int count, int reps, float* ms) {
   SG_CK(cudaEventCreate(&e0));
   SG_CK(cudaEventCreate(&e1));
   const int n = h->d.nt / 2;
-  auto body = [&](cudaStream_t s) {
+  auto body = [&](cudaStream_t s) -> int {
     if (which == 0 || which == 2) {
       FwdPlan p;
       if (which == 0) {
-        p.hist = h->hist;
-        p.hist_shot = (int64_t)h->hist_steps * h->hplane;
-        p.hist_n0 = n;
-        p.hist_mod = true;
-        p.hist_len = (int)h->hist_steps;
+        p.hist = main_hist(h, n);
+        p.hist.rotate = true;
       }
-      for (int r = 0; r < reps; ++r) enq_forward<T>(h, s, count, n + (r & 1), n + (r & 1) + 1, p);
+      for (int r = 0; r < reps; ++r) SG_TRY(enq_forward<T>(h, s, count, n + (r & 1), n + (r & 1) + 1, p));
     } else {
       AdjPlan p;
-      p.hist = h->hist;
-      p.hist_shot = (int64_t)h->hist_steps * h->hplane;
-      p.hist_n0 = n;
-      for (int r = 0; r < reps; ++r) enq_adjoint<T>(h, s, count, n + 1, n, p);
+      p.hist = main_hist(h, n);
+      for (int r = 0; r < reps; ++r) SG_TRY(enq_adjoint<T>(h, s, count, n + 1, n, p));
     }
+    return SG_OK;
   };
-  body(h->stream);  // warm-up
+  SG_TRY(body(h->stream));  // warm-up
   SG_CK(cudaEventRecord(e0, h->stream));
-  body(h->stream);
+  SG_TRY(body(h->stream));
   SG_CK(cudaEventRecord(e1, h->stream));
   SG_CK(cudaEventSynchronize(e1));
   float t = 0.f;
@@ -1072,7 +1181,7 @@ int sg_create(const sg_desc* d, sg_handle** out) {
   h->plane = (int64_t)(h->nzp + 2 * kGuard) * h->ldx;
   h->origin = (int64_t)kGuard * h->ldx;
   h->hplane = (int64_t)h->nzp * h->ldx;
-  h->tail = (int64_t)(kTileRowsMax + 2 * kGuard + 2) * h->ldx + 1024;
+  h->tail = (int64_t)(kTileRowsMax + 2 * kGuard + 4) * h->ldx;
   h->tiles_x = (h->nxp + BX - 1) / BX;
   h->ntiles = h->tiles_x * ((h->nzp + TH - 1) / TH);
   h->rec_blocks = (d->n_rec + RB - 1) / RB;
@@ -1100,7 +1209,7 @@ int sg_destroy(sg_handle* h) {
   if (!h) return SG_OK;
   cudaSetDevice(h->d.device);
   free_batch(h);
-  void** bufs[] = {&h->inv_m_buf, &h->pz_buf, &h->px_buf, &h->gscale_buf, (void**)&h->src_ij,
+  void** bufs[] = {&h->inv_m_buf, &h->pz_buf, &h->px_buf, &h->gscale_buf, (void**)&h->src_rc,
                    &h->src_w, (void**)&h->rec_ij, &h->rec_w, (void**)&h->inj_ptr,
                    (void**)&h->inj_rec, &h->inj_w, &h->born_hist};
   for (auto p : bufs) dfree(p);
@@ -1146,13 +1255,14 @@ int sg_set_geometry(sg_handle* h, const int32_t* src_rows, const int32_t* src_co
   auto in_grid = [&](int r, int c) { return r >= 0 && r < h->nzp && c >= 0 && c < h->nxp; };
   // sources: (4, S) -> per shot 4 flat offsets, weights * src_scale
   // (seisopt/wavesim.py:284: sw = src_w * src_scale)
-  std::vector<int> sij(4 * S);
+  std::vector<int> src(8 * S);
   std::vector<double> sw(4 * S);
   for (int s = 0; s < S; ++s)
     for (int k = 0; k < 4; ++k) {
       const int r = src_rows[k * S + s], c = src_cols[k * S + s];
       if (!in_grid(r, c)) return fail(SG_ERR_ARG, "source tap outside padded grid");
-      sij[s * 4 + k] = r * h->ldx + c;
+      src[(s * 4 + k) * 2] = r;
+      src[(s * 4 + k) * 2 + 1] = c;
       sw[s * 4 + k] = src_w[k * S + s] * src_scale;
     }
   std::vector<int> rij(4 * R);
@@ -1179,11 +1289,11 @@ int sg_set_geometry(sg_handle* h, const int32_t* src_rows, const int32_t* src_co
     irec[at] = e % R;
     iw[at] = rec_w[e];
   }
-  void** bufs[] = {(void**)&h->src_ij, &h->src_w, (void**)&h->rec_ij, &h->rec_w,
+  void** bufs[] = {(void**)&h->src_rc, &h->src_w, (void**)&h->rec_ij, &h->rec_w,
                    (void**)&h->inj_ptr, (void**)&h->inj_rec, &h->inj_w};
   for (auto p : bufs) dfree(p);
-  SG_TRY(dalloc(h, (void**)&h->src_ij, sij.size() * sizeof(int)));
-  SG_CK(cudaMemcpy(h->src_ij, sij.data(), sij.size() * sizeof(int), cudaMemcpyHostToDevice));
+  SG_TRY(dalloc(h, (void**)&h->src_rc, src.size() * sizeof(int)));
+  SG_CK(cudaMemcpy(h->src_rc, src.data(), src.size() * sizeof(int), cudaMemcpyHostToDevice));
   SG_TRY(dalloc(h, (void**)&h->rec_ij, rij.size() * sizeof(int)));
   SG_CK(cudaMemcpy(h->rec_ij, rij.data(), rij.size() * sizeof(int), cudaMemcpyHostToDevice));
   SG_TRY(dalloc(h, (void**)&h->inj_ptr, cnt.size() * sizeof(int)));

@@ -131,7 +131,7 @@ class Propagator:
 
     def __init__(self, grid, geometry, wavelet, config=SimConfig(), dtype="float64",
                  device=None, recon="auto", batch=0, checkpoint_every=0, use_graphs=True,
-                 mem_budget_bytes=0.0):
+                 mem_budget_bytes=0.0, group=0):
         torch = _torch()
         self.lib = _lib.load()
         if not torch.cuda.is_available():
@@ -159,6 +159,7 @@ class Propagator:
         d.batch, d.checkpoint_every = int(batch), int(checkpoint_every)
         d.device = self.device.index
         d.use_graphs = 1 if use_graphs else 0
+        d.group = int(group)
         d.dx, d.dz, d.dt = grid.dx, grid.dz, geometry.dt
         d.cfl_safety = config.cfl_safety
         d.mem_budget_bytes = float(mem_budget_bytes)

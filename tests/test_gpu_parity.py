@@ -252,3 +252,22 @@ def test_minimize_aa_trajectory_fp64():
                                   case["geometry"], case["config"])
     r0 = anderson.minimize_aa(obj0, g["m"].ravel(), memory=0, max_iters=3)
     assert rel(r0.p, gold["sd_final"]) <= F64
+
+
+@pytest.mark.parametrize("group", [1, 2, 3])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_shot_groups_agree(group, dtype):
+    """Different shots-per-CTA groupings give the same gradient (fp64: to
+    round-off of the image sum order)."""
+    _, wavesim = _api()
+    case = c1(8)
+    g = case["gold"]
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    st = oracle_setup(g["m_true"], grid, geom, cfg)
+    obs = np.stack(oracle.fwi_synthetic(st, wav.samples, geom.nt, threads=5))
+    p = wavesim.Propagator(grid, geom, wav, cfg, dtype=dtype, group=group)
+    p.set_model(g["m_init"])
+    v, gr = p.gradient(obs)
+    tol = F64 if dtype == "float64" else F32
+    assert abs(v - float(g["value"])) <= tol * float(g["value"])
+    assert rel(gr.cpu().numpy(), g["grad"]) <= tol
