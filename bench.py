@@ -184,6 +184,40 @@ def run_reference(args):
     return 0
 
 
+def run_reference_c2(args):
+    import oracle
+    rank, _, _ = env_rank()
+    if rank != 0:
+        return 0
+    nc, m, n = 5_000_000, 10, 50_000_000
+    rng = np.random.default_rng(0)
+    wo = oracle.AAWindowOracle(nc, m)
+    vecs = [(rng.standard_normal(nc), rng.standard_normal(nc))
+            for _ in range(m + 1 + args.warmup + args.steps)]
+    for k in range(m + 1 + args.warmup):
+        wo.push(*vecs[k])
+    times = []
+    for k in range(m + 1 + args.warmup, len(vecs)):
+        t0 = time.perf_counter()
+        wo.push(*vecs[k])
+        oracle.aa_step(wo, 1.0, oracle.aa_weights(wo))
+        times.append((time.perf_counter() - t0) * 1e3 * (n / nc))
+    v = statistics.median(times)
+    sample = f"AAWindow push+weights+step at N={nc} (scaled x{n // nc} to N=5e7), m={m}"
+    print(json.dumps({"impl": "reference", "metric": "AA mixing step time (push + weights + step)",
+                      "value": v, "unit": "ms/iteration", "n_gpus": args.gpus,
+                      "steps": args.steps, "warmup": args.warmup, "ms_per_step": v,
+                      "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+                      "dtype": "f64", "data": "synthetic",
+                      "config": {"workload": "C2 standalone AA mixing step", "sample": sample},
+                      "cpu_baseline": {"value": v, "unit": "ms/iteration",
+                                       "cores": os.cpu_count() or 1, "kind": "port",
+                                       "sample": sample},
+                      "e2e": {"value": v, "unit": "ms/iteration", "h2d_bytes_per_step": 0,
+                              "d2h_bytes_per_step": 0}}), flush=True)
+    return 0
+
+
 def workload_name(config):
     return {
         "c1": "C1 FWI gradient: 101x101, 5 shots, nt 800, 8th order, fp64",
@@ -335,15 +369,124 @@ def run_ours(args):
     return 0
 
 
+def aa_stream_torch(n, count, seed, dev, dtype):
+    """C2 stream on the device: N(0,1) vectors plus a shared smooth rank-3
+    component (BASELINE.json configs[1]); same recipe as synthetic.aa_window_stream."""
+    import torch
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    t = torch.linspace(0.0, 1.0, n, device=dev, dtype=torch.float64)
+    modes = [np.sqrt(2.0) * torch.sin(2.0 * np.pi * (j + 1) * t) for j in range(3)]
+    out = []
+    for _ in range(count):
+        pair = []
+        for _ in range(2):
+            v = torch.randn(n, generator=g, device=dev, dtype=torch.float64)
+            c = torch.randn(3, generator=g, device=dev, dtype=torch.float64)
+            for j in range(3):
+                v += c[j] * modes[j]
+            pair.append(v.to(dtype))
+        out.append(pair)
+    return out
+
+
+def run_c2(args):
+    """Standalone AA mixing step (configs[1]): N = 5e7 fp32, m = 10; one step =
+    push (fused residual-difference + Gram row pass) + host m x m solve +
+    recombination, window full and sliding."""
+    import torch
+
+    from paper_2008_11778_b200 import _lib, anderson
+    rank, world, local = env_rank()
+    if rank != 0:
+        return 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n, m = 50_000_000, 10
+    total = m + 1 + args.warmup + args.steps
+    stream = aa_stream_torch(n, total, 0, dev, torch.float32)
+    win = anderson.AAWindow(n, m, dtype="float32", device=dev)
+    out = torch.empty(n, device=dev, dtype=torch.float32)
+    for k in range(m + 1 + args.warmup):
+        win.push(*stream[k])
+        if win.m_k:
+            anderson.aa_step(win, weights=anderson.aa_weights(win), out=out)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        e0.record()
+        for k in range(m + 1 + args.warmup, total):
+            win.push(*stream[k])
+            w = anderson.aa_weights(win)
+            anderson.aa_step(win, weights=w, out=out)
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = _lib.launch_count() - l0
+    alg_bytes = 4.0 * n * (2 * m + 7)  # SURVEY s8d byte model
+    peak, src = peaks()
+    # e2e: host vectors in (pinned), host iterate out, every step
+    hp = [(a.cpu().pin_memory(), b.cpu().pin_memory()) for a, b in stream[-args.steps:]]
+    host_out = torch.empty(n, dtype=torch.float32).pin_memory()
+    pd, gd = torch.empty_like(out), torch.empty_like(out)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for a, b in hp:
+        pd.copy_(a, non_blocking=True)
+        gd.copy_(b, non_blocking=True)
+        win.push(pd, gd)
+        anderson.aa_step(win, weights=anderson.aa_weights(win), out=out)
+        host_out.copy_(out, non_blocking=True)
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / len(hp)
+    cpu = None
+    if not args.no_cpu:
+        import oracle
+        nc = 5_000_000
+        rng = np.random.default_rng(0)
+        wo = oracle.AAWindowOracle(nc, m)
+        vecs = [(rng.standard_normal(nc), rng.standard_normal(nc)) for _ in range(m + 3)]
+        for k in range(m + 1):
+            wo.push(*vecs[k])
+        t0 = time.perf_counter()
+        for k in range(m + 1, m + 3):
+            wo.push(*vecs[k])
+            oracle.aa_step(wo, 1.0, oracle.aa_weights(wo))
+        cms = (time.perf_counter() - t0) * 1e3 / 2 * (n / nc)
+        cpu = {"value": cms, "unit": "ms/iteration", "cores": os.cpu_count() or 1,
+               "kind": "port", "sample": f"oracle AAWindow push+weights+step at N={nc}, m={m}, "
+                                         "2 steady-state iterations, scaled x10 to N=5e7"}
+    line = {"metric": "AA mixing step time (push + weights + step)", "value": ms,
+            "unit": "ms/iteration", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C2 standalone AA mixing step: N=5e7 fp32, m=10, N(0,1) + "
+                                   "rank-3 smooth component", "l2": "inputs larger than L2 "
+                                   "(%.1f GB of window vectors)" % (2 * m * n * 4 / 1e9)},
+            "e2e": {"value": e2e_ms, "unit": "ms/iteration", "h2d_bytes_per_step": 2 * n * 4,
+                    "d2h_bytes_per_step": n * 4},
+            "roofline": {"bound": "hbm", "kernel": "aa_push + aa_step",
+                         "achieved": alg_bytes / (ms / 1e3) / 1e9, "peak": peak,
+                         "peak_source": src, "unit": "GB/s",
+                         "frac": alg_bytes / (ms / 1e3) / 1e9 / peak, "traffic": None,
+                         "bytes_per_launch": alg_bytes},
+            "gpu_launches": launches, "clocks": clk.summary(), "cpu_baseline": cpu}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c3", choices=["c1", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.config == "c2":
+        return run_c2(args) if args.impl != "reference" else run_reference_c2(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

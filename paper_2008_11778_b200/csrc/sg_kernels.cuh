@@ -157,6 +157,62 @@ __device__ __forceinline__ void bulk_wait0() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ---- paired arithmetic: two cells per instruction -------------------------
+// fp32 uses Blackwell's packed FADD2/FMUL2/FFMA2 (add/sub/mul/fma.rn.f32x2);
+// fp64 falls back to two scalar ops.  Results are bitwise those of the scalar
+// code (fma stays fused, rounding per op unchanged).
+template <typename T>
+struct V2;
+
+template <>
+struct V2<float> {
+  unsigned long long v;
+  __device__ __forceinline__ static V2 make(float a, float b) {
+    V2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
+    return r;
+  }
+  __device__ __forceinline__ void split(float& a, float& b) const {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  }
+  __device__ __forceinline__ friend V2 operator+(V2 a, V2 b) {
+    V2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+  }
+  __device__ __forceinline__ friend V2 operator-(V2 a, V2 b) {
+    V2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+  }
+  __device__ __forceinline__ friend V2 operator*(V2 a, V2 b) {
+    V2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+  }
+  __device__ __forceinline__ static V2 fma(V2 a, V2 b, V2 c) {
+    V2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+    return r;
+  }
+};
+
+template <>
+struct V2<double> {
+  double x, y;
+  __device__ __forceinline__ static V2 make(double a, double b) { return V2{a, b}; }
+  __device__ __forceinline__ void split(double& a, double& b) const {
+    a = x;
+    b = y;
+  }
+  __device__ __forceinline__ friend V2 operator+(V2 a, V2 b) { return V2{a.x + b.x, a.y + b.y}; }
+  __device__ __forceinline__ friend V2 operator-(V2 a, V2 b) { return V2{a.x - b.x, a.y - b.y}; }
+  __device__ __forceinline__ friend V2 operator*(V2 a, V2 b) { return V2{a.x * b.x, a.y * b.y}; }
+  __device__ __forceinline__ static V2 fma(V2 a, V2 b, V2 c) {
+    return V2{__fma_rn(a.x, b.x, c.x), __fma_rn(a.y, b.y, c.y)};
+  }
+};
+
 // shared-memory plan of one CTA (element counts; every region 128-B aligned):
 // two stages of {halo'd field tile, state tile[, history tile (adjoint)]}
 template <typename T, int R, bool ADJ>
@@ -309,53 +365,70 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? 3 : 2)
     const T* sst = st + SM::HALO + rb * kBX + threadIdx.x;
 
     if (nq > 0) {
+      using P = V2<T>;
+      constexpr int NH = kNY / 2;  // cells q and q + NH form one pair
       T col[NCOL];
 #pragma unroll
       for (int r = 0; r < NCOL; ++r) col[r] = sc[r * SW];
 #pragma unroll
-      for (int q = 0; q < kNY; ++q) {
-        if (q >= nq) break;
-        const T uc = col[q + R];
-        const T* row = sc + (q + R) * SW;
-        T lz = T(0), lx = T(0);
+      for (int q = 0; q < NH; ++q) {
+        // Laplacian of cells (q, q + NH) in difference form, two per instruction
+        const P uc = P::make(col[q + R], col[q + NH + R]);
+        const T* ra = sc + (q + R) * SW;
+        const T* rbw = sc + (q + NH + R) * SW;
+        P lz = P::make(T(0), T(0)), lx = P::make(T(0), T(0));
 #pragma unroll
         for (int kk = 1; kk <= R; ++kk) {
-          lz += a.cz[kk] * ((col[q + R - kk] - uc) + (col[q + R + kk] - uc));
-          lx += a.cx[kk] * ((row[-kk] - uc) + (row[kk] - uc));
+          const P cz = P::make(a.cz[kk], a.cz[kk]);
+          const P cx = P::make(a.cx[kk], a.cx[kk]);
+          const P zm = P::make(col[q + R - kk], col[q + NH + R - kk]);
+          const P zp = P::make(col[q + R + kk], col[q + NH + R + kk]);
+          const P xm = P::make(ra[-kk], rbw[-kk]);
+          const P xp = P::make(ra[kk], rbw[kk]);
+          lz = P::fma(cz, (zm - uc) + (zp - uc), lz);
+          lx = P::fma(cx, (xm - uc) + (xp - uc), lx);
         }
-        T lap = lz + lx;
-        const T sv = sst[q * kBX];
-        if (!ADJ) {
-          if (GSRC) lap += gin[q * ldx] * a.gscale[o0 + q * ldx];
-          T acc = lap * im[q];
-          if (src_here) {
-            const int i = ib + q;
+        T lap[2], ucs[2];
+        (lz + lx).split(lap[0], lap[1]);
+        uc.split(ucs[0], ucs[1]);
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              const int r = a.src_rc[(b * 4 + t) * 2], c = a.src_rc[(b * 4 + t) * 2 + 1];
-              if (r == i && c == j) acc += a.amp * a.src_w[b * 4 + t] * im[q];
+        for (int h = 0; h < 2; ++h) {
+          const int qq = q + h * NH;
+          if (qq >= nq) continue;
+          const T sv = sst[qq * kBX];
+          T lp = lap[h];
+          if (!ADJ) {
+            if (GSRC) lp += gin[qq * ldx] * a.gscale[o0 + qq * ldx];
+            T acc = lp * im[qq];
+            if (src_here) {
+              const int i = ib + qq;
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const int r = a.src_rc[(b * 4 + t) * 2], c = a.src_rc[(b * 4 + t) * 2 + 1];
+                if (r == i && c == j) acc += a.amp * a.src_w[b * 4 + t] * im[qq];
+              }
             }
-          }
-          if (HIST) hout[q * ldx] = acc;
-          const T so = dd[q] * (sv + a.dt2 * acc);
-          sout[q * ldx] = so;
-          fout[q * ldx] = dd[q] * uc + so;
-        } else {
-          if (inj_here) {
-            const int rr = ib + q - a.inj_row0;
-            if (rr >= 0 && rr < a.inj_nrows) {
-              // R^T y: duplicate taps accumulate (np.add.at, seisopt/wavesim.py:229)
-              const int cell = rr * a.nxp + j;
-              const int p1 = a.inj_ptr[cell + 1];
-              for (int p = a.inj_ptr[cell]; p < p1; ++p)
-                lap += a.inj_w[p] * a.ybar[(int64_t)b * a.ybar_stride + a.inj_rec[p]];
+            if (HIST) hout[qq * ldx] = acc;
+            const T so = dd[qq] * (sv + a.dt2 * acc);
+            sout[qq * ldx] = so;
+            fout[qq * ldx] = dd[qq] * ucs[h] + so;
+          } else {
+            if (inj_here) {
+              const int rr = ib + qq - a.inj_row0;
+              if (rr >= 0 && rr < a.inj_nrows) {
+                // R^T y: duplicate taps accumulate (np.add.at, seisopt/wavesim.py:229)
+                const int cell = rr * a.nxp + j;
+                const int p1 = a.inj_ptr[cell + 1];
+                for (int p = a.inj_ptr[cell]; p < p1; ++p)
+                  lp += a.inj_w[p] * a.ybar[(int64_t)b * a.ybar_stride + a.inj_rec[p]];
+              }
             }
+            const T so = dd[qq] * sv + lp;
+            sout[qq * ldx] = so;
+            fout[qq * ldx] = dd[qq] * ucs[h] + (a.dt2 * im[qq] * dd[qq]) * so;
+            if (LOAD_HIST) img[qq] -= sst[qq * kBX + SM::TILE] * ucs[h];
+            if (VHIST) a.vhist[(int64_t)b * a.vhist_stride + o0 + qq * ldx] = ucs[h];
           }
-          const T so = dd[q] * sv + lap;
-          sout[q * ldx] = so;
-          fout[q * ldx] = dd[q] * uc + (a.dt2 * im[q] * dd[q]) * so;
-          if (LOAD_HIST) img[q] -= sst[q * kBX + SM::TILE] * uc;
-          if (VHIST) a.vhist[(int64_t)b * a.vhist_stride + o0 + q * ldx] = uc;
         }
       }
     }

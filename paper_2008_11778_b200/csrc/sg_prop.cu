@@ -485,12 +485,11 @@ template <typename T, int R, bool ADJ>
 void launch_step_r(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a) {
   const int fl = (a.hist_on ? FL_HIST : 0) | (a.gsrc ? FL_GSRC : 0) |
                  (a.vhist ? FL_VHIST : 0) | (a.gather ? FL_GATHER : 0);
-  if (ADJ) {
+  if constexpr (ADJ) {
     if (fl & FL_VHIST) launch_step_f<T, R, ADJ, FL_VHIST>(h, s, a);
     else if (fl & FL_HIST) launch_step_f<T, R, ADJ, FL_HIST>(h, s, a);
     else launch_step_f<T, R, ADJ, 0>(h, s, a);
-    return;
-  }
+  } else {
   switch (fl & (FL_HIST | FL_GSRC | FL_GATHER)) {
     case 0: launch_step_f<T, R, ADJ, 0>(h, s, a); break;
     case FL_HIST: launch_step_f<T, R, ADJ, FL_HIST>(h, s, a); break;
@@ -500,6 +499,7 @@ void launch_step_r(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a) {
     case FL_GSRC | FL_GATHER: launch_step_f<T, R, ADJ, FL_GSRC | FL_GATHER>(h, s, a); break;
     case FL_GSRC | FL_HIST: launch_step_f<T, R, ADJ, FL_GSRC | FL_HIST>(h, s, a); break;
     default: launch_step_f<T, R, ADJ, FL_GSRC | FL_HIST | FL_GATHER>(h, s, a); break;
+  }
   }
 }
 

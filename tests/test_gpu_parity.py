@@ -271,3 +271,60 @@ def test_shot_groups_agree(group, dtype):
     tol = F64 if dtype == "float64" else F32
     assert abs(v - float(g["value"])) <= tol * float(g["value"])
     assert rel(gr.cpu().numpy(), g["grad"]) <= tol
+
+
+def test_aa_window_fp32_at_scale_vs_fp64_oracle():
+    """C2-distribution window (N=1e6, m=10): fp32 device window vs the fp64
+    reference algorithm (oracle pinned to seisopt) on the same inputs."""
+    from paper_2008_11778_b200 import anderson, synthetic
+    n, m = 1_000_000, 10
+    win = anderson.AAWindow(n, m, dtype="float32")
+    ref = oracle.AAWindowOracle(n, m)
+    for k, (p, g) in enumerate(synthetic.aa_window_stream(n, 2 * m + 3, seed=1)):
+        win.push(torch.as_tensor(p, device="cuda"), torch.as_tensor(g, device="cuda"))
+        ref.push(p.astype(np.float64), g.astype(np.float64))
+        assert win.m_k == ref.m_k
+        if ref.m_k:
+            w = anderson.aa_weights(win)
+            gr, ar, rr = oracle.aa_weights(ref)
+            assert rel(w.gamma, gr) <= 1e-6
+            assert abs(w.residual_norm - rr) <= 1e-5 * rr
+            step = anderson.aa_step(win, weights=w).double().cpu().numpy()
+            assert rel(step, oracle.aa_step(ref, 1.0, (gr, ar, rr))) <= 1e-6
+
+
+def test_c3_single_shot_fp32_gradient():
+    """C3 grid (201x601, 8th order, nt 4000), one shot: fp32 device gradient
+    vs the fp64 oracle."""
+    from paper_2008_11778_b200 import synthetic, wavesim
+    from paper_2008_11778_b200.model import AcquisitionGeometry
+    case = synthetic.layered_case("c3")
+    geom0 = case["geometry"]
+    geom = AcquisitionGeometry((geom0.sources[11],), geom0.receivers, geom0.dt, geom0.nt)
+    grid, cfg, wav = case["grid"], case["config"], case["wavelet"]
+    st_true = oracle_setup(case["true"].m, grid, geom, cfg)
+    obs = oracle.fwi_synthetic(st_true, wav.samples, geom.nt)
+    st = oracle_setup(case["init"].m, grid, geom, cfg)
+    val, grad, _ = oracle.fwi_gradient(st, obs, wav.samples, geom.nt)
+    prop = wavesim.Propagator(grid, geom, wav, cfg, dtype="float32")
+    prop.set_model(case["init"].m)
+    v, g = prop.gradient(np.stack(obs))
+    assert abs(v - val) <= F32 * val
+    assert rel(g.cpu().numpy(), grad) <= F32
+
+
+def test_c1_fp32_aa_misfit_curve():
+    """fp32 production path: the misfit-vs-iteration curve of 20 AA
+    iterations (m=5) stays within 1% of the reference's fp64 run."""
+    from paper_2008_11778_b200 import anderson, gradients
+    case = c1(8)
+    g = case["gold"]
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    st = oracle_setup(g["m_true"], grid, geom, cfg)
+    obs = np.stack(oracle.fwi_synthetic(st, wav.samples, geom.nt, threads=5))
+    obj = gradients.FwiObjective(grid, obs, wav, geom, cfg, dtype="float32")
+    res = anderson.minimize_aa(obj, g["m_init"].ravel(), memory=5, max_iters=20)
+    mine = np.array([r.objective for r in res.report.rows])
+    ref = g["aa_rows"][:, 1]
+    assert mine.shape == ref.shape
+    assert np.max(np.abs(mine - ref) / ref) <= 0.01
