@@ -29,13 +29,37 @@ namespace {
 
 constexpr int kMaxMem = 32;  // largest supported AA memory
 constexpr int kThreads = 256;
-constexpr int kBlocks = 148 * 4;
+constexpr int kBlocks = 148 * 8;
 
 struct Slots {
   int s[kMaxMem];
 };
 struct Coefs {
   double c[kMaxMem];
+};
+
+// 16-byte vectors: 4 floats or 2 doubles per load
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+  using type = float4;
+  static constexpr int W = 4;
+  __device__ __forceinline__ static float get(const float4& v, int l) {
+    return l == 0 ? v.x : l == 1 ? v.y : l == 2 ? v.z : v.w;
+  }
+  __device__ __forceinline__ static void set(float4& v, int l, float x) {
+    if (l == 0) v.x = x; else if (l == 1) v.y = x; else if (l == 2) v.z = x; else v.w = x;
+  }
+};
+template <>
+struct Vec<double> {
+  using type = double2;
+  static constexpr int W = 2;
+  __device__ __forceinline__ static double get(const double2& v, int l) { return l == 0 ? v.x : v.y; }
+  __device__ __forceinline__ static void set(double2& v, int l, double x) {
+    if (l == 0) v.x = x; else v.y = x;
+  }
 };
 
 // fused push: f_k = g - p; df = f_k - f_prev; dg = g - g_prev; store df, dg
@@ -46,43 +70,89 @@ struct Coefs {
 //   2nw+1          <f_k, df>
 //   2nw+2          <f_k, f_k>
 // first != 0: only f_prev/g_prev are written and <f_k, f_k> reduced.
-template <typename T, int MW>
+// Element k of the vectorised loop covers elements [k*W, k*W + W); the tail
+// n % W (and every element when VEC is false) runs the scalar loop.
+template <typename T, int MW, bool VEC>
 __global__ void __launch_bounds__(kThreads)
     k_aa_push(const T* __restrict__ p, const T* __restrict__ g, T* __restrict__ fprev,
               T* __restrict__ gprev, T* __restrict__ DF, T* __restrict__ DG, int64_t n,
-              const Slots slots, int nw, int snew, int first, double* __restrict__ part) {
+              int64_t ld, const Slots slots, int nw, int snew, int first,
+              double* __restrict__ part) {
+  using VT = Vec<T>;
+  using V = typename VT::type;
+  constexpr int W = VEC ? VT::W : 1;
   double a_dd[MW], a_fd[MW];
 #pragma unroll
   for (int i = 0; i < MW; ++i) a_dd[i] = a_fd[i] = 0.0;
   double dd = 0.0, fd = 0.0, ff = 0.0;
-  T* dfn = DF + (int64_t)snew * n;
-  T* dgn = DG + (int64_t)snew * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const T gv = g[e];
-    const T fk = gv - p[e];  // seisopt/optim/anderson.py:84
-    const double fkd = (double)fk;
-    ff += fkd * fkd;
-    if (first) {
-      fprev[e] = fk;
-      gprev[e] = gv;
-      continue;
+  T* dfn = DF + (int64_t)snew * ld;
+  T* dgn = DG + (int64_t)snew * ld;
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nv = n / W;
+  auto body = [&](T gv, T pv, T fpv, T gpv, T& df_out, T& dg_out, T& fk_out) {
+    const T fk = gv - pv;  // seisopt/optim/anderson.py:84
+    const T df = fk - fpv; // anderson.py:89
+    df_out = df;
+    dg_out = gv - gpv;     // anderson.py:90
+    fk_out = fk;
+  };
+  if (VEC) {
+    for (int64_t e = gtid; e < nv; e += gstride) {
+      const V gv = reinterpret_cast<const V*>(g)[e];
+      const V pv = reinterpret_cast<const V*>(p)[e];
+      V fpv = reinterpret_cast<const V*>(fprev)[e];
+      V gpv = reinterpret_cast<const V*>(gprev)[e];
+      V dfv, dgv, fkv;
+#pragma unroll
+      for (int l = 0; l < W; ++l) {
+        T df, dg, fk;
+        body(VT::get(gv, l), VT::get(pv, l), VT::get(fpv, l), VT::get(gpv, l), df, dg, fk);
+        VT::set(dfv, l, df);
+        VT::set(dgv, l, dg);
+        VT::set(fkv, l, fk);
+        ff += (double)fk * (double)fk;
+        if (!first) {
+          dd += (double)df * (double)df;
+          fd += (double)fk * (double)df;
+        }
+      }
+      reinterpret_cast<V*>(fprev)[e] = fkv;
+      reinterpret_cast<V*>(gprev)[e] = gv;
+      if (first) continue;
+      reinterpret_cast<V*>(dfn)[e] = dfv;
+      reinterpret_cast<V*>(dgn)[e] = dgv;
+#pragma unroll
+      for (int i = 0; i < MW; ++i) {
+        if (i < nw) {
+          const V c = reinterpret_cast<const V*>(DF + (int64_t)slots.s[i] * ld)[e];
+#pragma unroll
+          for (int l = 0; l < W; ++l) {
+            const double cv = (double)VT::get(c, l);
+            a_dd[i] += (double)VT::get(dfv, l) * cv;
+            a_fd[i] += (double)VT::get(fkv, l) * cv;
+          }
+        }
+      }
     }
-    const T df = fk - fprev[e];  // anderson.py:89
-    const T dg = gv - gprev[e];  // anderson.py:90
+  }
+  for (int64_t e = nv * W + gtid; e < n; e += gstride) {
+    T df, dg, fk;
+    body(g[e], p[e], fprev[e], gprev[e], df, dg, fk);
+    fprev[e] = fk;
+    gprev[e] = g[e];
+    ff += (double)fk * (double)fk;
+    if (first) continue;
     dfn[e] = df;
     dgn[e] = dg;
-    fprev[e] = fk;
-    gprev[e] = gv;
-    const double dfd = (double)df;
-    dd += dfd * dfd;
-    fd += fkd * dfd;
+    dd += (double)df * (double)df;
+    fd += (double)fk * (double)df;
 #pragma unroll
     for (int i = 0; i < MW; ++i) {
       if (i < nw) {
-        const double c = (double)DF[(int64_t)slots.s[i] * n + e];
-        a_dd[i] += dfd * c;
-        a_fd[i] += fkd * c;
+        const double c = (double)DF[(int64_t)slots.s[i] * ld + e];
+        a_dd[i] += (double)df * c;
+        a_fd[i] += (double)fk * c;
       }
     }
   }
@@ -127,31 +197,61 @@ __global__ void k_sum_cols(const double* __restrict__ part, int nb, int na,
 //   beta == 1: out = G_k - sum_i gamma_i dG_i
 //   else     : out = (1-beta) (p_k - sum gamma_i (dG_i - dF_i)) + beta (G_k - sum gamma_i dG_i)
 //              (sum_i alpha_i x_i = x_k - sum_i gamma_i dx_i, p = G - f)
-template <typename T, int MW>
+template <typename T, int MW, bool VEC>
 __global__ void __launch_bounds__(kThreads)
     k_aa_step(const T* __restrict__ gk, const T* __restrict__ fk, const T* __restrict__ DF,
-              const T* __restrict__ DG, int64_t n, const Slots slots, int nw, const Coefs gam,
-              double beta, T* __restrict__ out) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    double acc = (double)gk[e];
-    if (beta == 1.0) {
+              const T* __restrict__ DG, int64_t n, int64_t ld, const Slots slots, int nw,
+              const Coefs gam, double beta, T* __restrict__ out) {
+  using VT = Vec<T>;
+  using V = typename VT::type;
+  constexpr int W = VEC ? VT::W : 1;
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nv = n / W;
+  if (VEC) {
+    for (int64_t e = gtid; e < nv; e += gstride) {
+      const V gv = reinterpret_cast<const V*>(gk)[e];
+      double acc[W], cp[W];
 #pragma unroll
-      for (int i = 0; i < MW; ++i)
-        if (i < nw) acc -= gam.c[i] * (double)DG[(int64_t)slots.s[i] * n + e];
-      out[e] = (T)acc;
-    } else {
-      double cp = acc - (double)fk[e];
+      for (int l = 0; l < W; ++l) acc[l] = (double)VT::get(gv, l);
+      if (beta != 1.0) {
+        const V fv = reinterpret_cast<const V*>(fk)[e];
 #pragma unroll
-      for (int i = 0; i < MW; ++i)
+        for (int l = 0; l < W; ++l) cp[l] = acc[l] - (double)VT::get(fv, l);
+      }
+#pragma unroll
+      for (int i = 0; i < MW; ++i) {
         if (i < nw) {
-          const double dg = (double)DG[(int64_t)slots.s[i] * n + e];
-          const double df = (double)DF[(int64_t)slots.s[i] * n + e];
-          acc -= gam.c[i] * dg;
-          cp -= gam.c[i] * (dg - df);
+          const V dg = reinterpret_cast<const V*>(DG + (int64_t)slots.s[i] * ld)[e];
+#pragma unroll
+          for (int l = 0; l < W; ++l) acc[l] -= gam.c[i] * (double)VT::get(dg, l);
+          if (beta != 1.0) {
+            const V df = reinterpret_cast<const V*>(DF + (int64_t)slots.s[i] * ld)[e];
+#pragma unroll
+            for (int l = 0; l < W; ++l)
+              cp[l] -= gam.c[i] * ((double)VT::get(dg, l) - (double)VT::get(df, l));
+          }
         }
-      out[e] = (T)((1.0 - beta) * cp + beta * acc);
+      }
+      V o;
+#pragma unroll
+      for (int l = 0; l < W; ++l)
+        VT::set(o, l, (T)(beta == 1.0 ? acc[l] : (1.0 - beta) * cp[l] + beta * acc[l]));
+      reinterpret_cast<V*>(out)[e] = o;
     }
+  }
+  for (int64_t e = nv * W + gtid; e < n; e += gstride) {
+    double acc = (double)gk[e];
+    double cp = acc - (double)fk[e];
+#pragma unroll
+    for (int i = 0; i < MW; ++i)
+      if (i < nw) {
+        const double dg = (double)DG[(int64_t)slots.s[i] * ld + e];
+        const double df = (double)DF[(int64_t)slots.s[i] * ld + e];
+        acc -= gam.c[i] * dg;
+        cp -= gam.c[i] * (dg - df);
+      }
+    out[e] = (T)(beta == 1.0 ? acc : (1.0 - beta) * cp + beta * acc);
   }
 }
 
@@ -240,6 +340,8 @@ __global__ void k_stats(int64_t n, const T* __restrict__ x, double* __restrict__
   }
 }
 
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(kBlocks, (n + kThreads - 1) / kThreads)); }
 
 // exactly rounded sum (Shewchuk partials, as Python's math.fsum)
@@ -282,6 +384,7 @@ double fsum(const std::vector<double>& xs) {
 
 struct sg_aa {
   int64_t n = 0;
+  int64_t ld = 0;  // slot stride (n rounded up to 64 elements, keeps columns 256-B aligned)
   int memory = 0;
   int esz = 8;
   int device = 0;
@@ -423,9 +526,21 @@ int push_t(sg_aa* a, const void* p, const void* g) {
   T* fk = reinterpret_cast<T*>(a->fk);
   T* gk = reinterpret_cast<T*>(a->gk);
   const int mw = std::max(nw, 1);
-#define PUSH(MW) k_aa_push<T, MW><<<nb, kThreads, 0, a->stream>>>(pp, gg, fk, gk, DF, DG, a->n, sl, nw, snew, first, a->part)
+  const bool vec = aligned16(pp) && aligned16(gg);
+#define PUSH(MW)                                                                              \
+  do {                                                                                        \
+    if (vec)                                                                                  \
+      k_aa_push<T, MW, true><<<nb, kThreads, 0, a->stream>>>(pp, gg, fk, gk, DF, DG, a->n, \
+                                                              a->ld, sl, nw, snew, first,    \
+                                                              a->part);                      \
+    else                                                                                      \
+      k_aa_push<T, MW, false><<<nb, kThreads, 0, a->stream>>>(pp, gg, fk, gk, DF, DG, a->n, \
+                                                               a->ld, sl, nw, snew, first,   \
+                                                               a->part);                     \
+  } while (0)
   if (mw <= 4) PUSH(4);
   else if (mw <= 8) PUSH(8);
+  else if (mw <= 12) PUSH(12);
   else if (mw <= 16) PUSH(16);
   else PUSH(32);
 #undef PUSH
@@ -477,9 +592,19 @@ int step_t(sg_aa* a, double beta, const double* gamma, void* out) {
   const T* DG = reinterpret_cast<const T*>(a->DG);
   T* o = reinterpret_cast<T*>(out);
   const int mw = std::max(k, 1);
-#define STEP(MW) k_aa_step<T, MW><<<nb, kThreads, 0, a->stream>>>(gk, fk, DF, DG, a->n, sl, k, cf, beta, o)
+  const bool vec = aligned16(o);
+#define STEP(MW)                                                                               \
+  do {                                                                                         \
+    if (vec)                                                                                   \
+      k_aa_step<T, MW, true><<<nb, kThreads, 0, a->stream>>>(gk, fk, DF, DG, a->n, a->ld, sl, \
+                                                              k, cf, beta, o);                \
+    else                                                                                       \
+      k_aa_step<T, MW, false><<<nb, kThreads, 0, a->stream>>>(gk, fk, DF, DG, a->n, a->ld,   \
+                                                               sl, k, cf, beta, o);           \
+  } while (0)
   if (mw <= 4) STEP(4);
   else if (mw <= 8) STEP(8);
+  else if (mw <= 12) STEP(12);
   else if (mw <= 16) STEP(16);
   else STEP(32);
 #undef STEP
@@ -505,7 +630,8 @@ int sg_aa_create(int64_t n, int32_t memory, int32_t dtype, int32_t device, sg_aa
   a->memory = memory;
   a->esz = dtype;
   a->device = device;
-  const size_t vb = (size_t)n * dtype;
+  a->ld = (n + 63) / 64 * 64;
+  const size_t vb = (size_t)a->ld * dtype;
   const int slots = std::max(memory, 1);
   cudaError_t e = cudaMalloc(&a->DF, vb * slots);
   if (e == cudaSuccess) e = cudaMalloc(&a->DG, vb * slots);
