@@ -115,17 +115,26 @@ __global__ void k_model_stats(const M* __restrict__ m, int64_t n, double* __rest
 //   mode 2 (value): no ybar,               acc w_t (f-g)^2   (seisopt/gradients.py:70-79)
 template <typename T>
 __global__ void k_residual(const T* __restrict__ f, const T* __restrict__ g, T* ybar,
-                           int64_t total, int nt, int nrec, double dt, int mode,
+                           int64_t rows, int nt, int nrec, double dt, int mode,
                            double* __restrict__ part) {
+  // rows = shots * nt time samples; each block walks a contiguous run of rows
   double acc = 0.0;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int n = (int)((k / nrec) % nt);
-    const T r = f[k] - g[k];
+  const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = blockIdx.x * per;
+  const int64_t r1 = min(rows, r0 + per);
+  for (int64_t row = r0; row < r1; ++row) {
+    const int n = (int)(row % nt);
     const double w = (mode == 1) ? 1.0 : ((n == 0 || n == nt - 1) ? 0.5 : 1.0);
-    acc += w * (double)r * (double)r;
-    if (mode == 0) ybar[k] = (T)(w * dt) * r;
-    else if (mode == 1) ybar[k] = r;
+    const T wdt = (T)(w * dt);
+    const int64_t base = row * nrec;
+    double racc = 0.0;
+    for (int r = threadIdx.x; r < nrec; r += blockDim.x) {
+      const T res = f[base + r] - g[base + r];
+      racc += (double)res * (double)res;
+      if (mode == 0) ybar[base + r] = wdt * res;
+      else if (mode == 1) ybar[base + r] = res;
+    }
+    acc += w * racc;
   }
   const double s = block_sum(acc);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
@@ -703,10 +712,10 @@ int zero_fields(sg_handle* h, bool fwd, bool adj, int cnt) {
 
 template <typename T>
 int residual(sg_handle* h, int cnt, const T* obs, int mode) {
-  const int64_t total = (int64_t)cnt * h->d.nt * h->d.n_rec;
-  const int blocks = std::min<int64_t>(h->npart, cdiv(total, 256));
+  const int64_t rows = (int64_t)cnt * h->d.nt;
+  const int blocks = (int)std::min<int64_t>(h->npart, rows);
   k_residual<T><<<blocks, 256, 0, h->stream>>>(reinterpret_cast<const T*>(h->gath), obs,
-                                               reinterpret_cast<T*>(h->gath), total, h->d.nt,
+                                               reinterpret_cast<T*>(h->gath), rows, h->d.nt,
                                                h->d.n_rec, h->d.dt, mode, h->part);
   const double scale = (mode == 1) ? 0.5 : 0.5 * h->d.dt;
   k_finish_sum<<<1, 1024, 0, h->stream>>>(h->part, blocks, scale, h->scal);
