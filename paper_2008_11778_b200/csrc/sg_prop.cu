@@ -248,7 +248,8 @@ struct sg_handle {
   int recon = SG_RECON_FULL;
   int K = 0, ncp = 0;     // checkpoint interval / count
   int64_t hist_steps = 0; // steps of history held per shot
-  int G = 1;              // shots per CTA group
+  int G = 0;              // set once batch buffers exist; see group_for()
+  int nsm = 148;          // SMs of the device
   int* bsrc_rc = nullptr;
   void* bsrc_w = nullptr;
   std::map<std::string, CUtensorMap> tmaps;  // TMA descriptors by buffer/kind
@@ -349,15 +350,7 @@ int ensure_batch(sg_handle* h) {
     return fail(SG_ERR_OOM, "one shot needs " + std::to_string(per / 1e9) +
                                 " GB of device memory; budget " + std::to_string(budget / 1e9));
   h->B = B;
-  // shots per CTA group: model data and the image accumulator are amortised
-  // over G shots; keep >= ~3 CTAs per SM
-  int G = h->d.group;
-  if (G <= 0) {
-    const char* e = getenv("SG_GROUP");
-    G = e ? atoi(e) : 0;
-  }
-  if (G <= 0) G = (int)std::floor((double)B * h->ntiles / (148.0 * 3.0));
-  h->G = std::max(1, std::min({G, 8, B}));
+  h->G = 1;  // group size is chosen per launch (group_for)
   h->recon = recon;
   h->K = K;
   h->ncp = ncp;
@@ -388,7 +381,38 @@ int ensure_batch(sg_handle* h) {
 // kernel argument builders + launchers
 // ---------------------------------------------------------------------------
 
-int ngroups(const sg_handle* h, int count) { return (count + h->G - 1) / h->G; }
+// Shots per CTA group for a launch over `count` shots.  Larger G amortises
+// the per-cell model reads and the image read-modify-write (~12 B/G of the
+// ~20 B per shot-cell); the persistent grid holds `slots` CTAs, so the
+// busiest CTA processes ceil(items / slots) * G shots.  Minimise that
+// critical path times the amortisation overhead.
+int group_for(const sg_handle* h, int count) {
+  if (h->d.group > 0) return std::max(1, std::min(h->d.group, count));
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("SG_GROUP");
+    env = e ? std::max(0, atoi(e)) : 0;
+  }
+  if (env > 0) return std::max(1, std::min(env, count));
+  const int slots = h->nsm * (h->esz == 4 ? 3 : 2);
+  int best = 1;
+  double best_cost = 1e300;
+  for (int G = 1; G <= std::min(8, count); ++G) {
+    const int64_t items = (int64_t)h->ntiles * ((count + G - 1) / G);
+    const double rounds = (double)((items + slots - 1) / slots);
+    const double cost = rounds * G * (1.0 + 0.6 / G);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = G;
+    }
+  }
+  return best;
+}
+
+int ngroups(const sg_handle* h, int count) {
+  const int G = group_for(h, count);
+  return (count + G - 1) / G;
+}
 
 // TMA descriptors.  Guarded buffers (fields, state) are viewed as 3-D
 // {ldx, nzp + 2 kGuard, B} starting after the lead row; histories as
@@ -476,7 +500,7 @@ int step_args(sg_handle* h, StepArgs<T>& a, void* F0, void* F1, void* state, voi
 }
 
 template <typename T, int R, bool ADJ, int FL>
-void launch_step_f(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a) {
+void launch_step_f(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a0) {
   static bool attr = false;
   constexpr int smem = step_smem_bytes<T, R, ADJ>();
   if (!attr) {
@@ -484,6 +508,9 @@ void launch_step_f(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a) {
                          smem);
     attr = true;
   }
+  StepArgs<T> a = a0;
+  a.G = group_for(h, a.count);
+  a.rec_blocks = (a.G * h->d.n_rec + RB - 1) / RB;
   const int extra = (!ADJ && (FL & FL_GATHER)) ? a.rec_blocks : 0;
   dim3 grid(h->ntiles + extra, ngroups(h, a.count)), block(kBX, kBY);
   k_step<T, R, ADJ, FL><<<grid, block, smem, s>>>(a);
@@ -1194,6 +1221,7 @@ int sg_create(const sg_desc* d, sg_handle** out) {
   h->tiles_x = (h->nxp + BX - 1) / BX;
   h->ntiles = h->tiles_x * ((h->nzp + TH - 1) / TH);
   h->rec_blocks = (d->n_rec + RB - 1) / RB;
+  cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, d->device);
   const double rz = 1.0 / (d->dz * d->dz), rx = 1.0 / (d->dx * d->dx);
   if (d->order == 2) {
     h->cz[1] = rz;
