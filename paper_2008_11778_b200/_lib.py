@@ -103,7 +103,7 @@ def load(path: str | None = None):
     with _lock:
         if _lib is not None:
             return _lib
-        p = path or LIB_PATH
+        p = path or os.environ.get("SG_LIB") or LIB_PATH
         if not os.path.exists(p):
             raise RuntimeError(
                 f"libseisgpu.so not built at {p}; run `python -m paper_2008_11778_b200.build` "

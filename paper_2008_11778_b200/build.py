@@ -41,18 +41,21 @@ def needs_rebuild():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_rebuild():
+def build(force=False, verbose=False, out=None, defines=()):
+    """Compile csrc/*.cu into `out` (default: the in-tree libseisgpu.so)."""
+    lib = out or LIB
+    if out is None and not force and not needs_rebuild():
         return LIB
     nvcc = nvcc_path()
     cmd = [nvcc, "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-O3",
-           "-shared", "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *sources()]
+           "-shared", "-I", os.path.join(ROOT, "include"), *[f"-D{d}" for d in defines],
+           "-o", lib + ".tmp", *sources()]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -41,6 +41,9 @@ constexpr int kBX = 64, kBY = 4, kNY = 8, kTH = kBY * kNY;  // 64 x 32 tile, 256
 // stencil reads the inner ring only.  72 x 40 boxes keep every TMA row a
 // multiple of 16 B for fp32 and fp64.
 constexpr int kHalo = 4;
+#ifndef SG_FP32_MINB
+#define SG_FP32_MINB 3
+#endif
 
 template <typename T>
 struct StepArgs {
@@ -241,7 +244,7 @@ constexpr int FL_VHIST = 4;   // ADJ: store v_n (adjoint_solve keep_v)
 constexpr int FL_GATHER = 8;  // FWD: receiver sampling blocks present
 
 template <typename T, int R, bool ADJ, int FL>
-__global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? 3 : 2)
+__global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
     k_step(const __grid_constant__ StepArgs<T> a) {
   using SM = Smem<T, R, ADJ>;
   constexpr int SW = SM::SW;
