@@ -67,7 +67,10 @@ typedef struct sg_desc {
   int32_t device;                    /* CUDA ordinal */
   int32_t use_graphs;                /* capture time loops in CUDA graphs (1) */
   int32_t group;                     /* shots per CTA group, 0 = auto */
-  int32_t reserved[3];
+  int32_t step_mode;                 /* 0 = auto (one step per launch), 1 = one
+                                        step, 2 = two steps per launch (fp32,
+                                        temporally blocked) */
+  int32_t reserved[2];
   double dx, dz, dt;                 /* metres, seconds */
   double cfl_safety;                 /* SimConfig.cfl_safety, seisopt/wavesim.py:57 */
   double mem_budget_bytes;           /* 0 = 90% of free device memory */
@@ -162,7 +165,8 @@ int sg_adjoint_history(sg_handle* h, const void* ybar_dev, void* v_dev);
 int sg_query(sg_handle* h, int32_t* batch, int32_t* recon, double* device_bytes);
 
 /* Times `reps` launches of one step kernel (0 = forward+history store,
- * 1 = adjoint+imaging, 2 = forward no history) over `count` shots with CUDA
+ * 1 = adjoint+imaging, 2 = forward no history; 3 / 4 = the two-step forward /
+ * adjoint kernels, two time steps per launch) over `count` shots with CUDA
  * events on the handle's stream; *ms_per_launch = mean duration. */
 int sg_time_step_kernel(sg_handle* h, int32_t which, int32_t count, int32_t reps,
                         float* ms_per_launch);

@@ -42,7 +42,8 @@ class SgDesc(C.Structure):
         ("nt", C.c_int32), ("n_shots", C.c_int32), ("n_rec", C.c_int32),
         ("dtype", C.c_int32), ("order", C.c_int32), ("recon", C.c_int32),
         ("batch", C.c_int32), ("checkpoint_every", C.c_int32), ("device", C.c_int32),
-        ("use_graphs", C.c_int32), ("group", C.c_int32), ("reserved", C.c_int32 * 3),
+        ("use_graphs", C.c_int32), ("group", C.c_int32), ("step_mode", C.c_int32),
+        ("reserved", C.c_int32 * 2),
         ("dx", C.c_double), ("dz", C.c_double), ("dt", C.c_double),
         ("cfl_safety", C.c_double), ("mem_budget_bytes", C.c_double),
     ]

@@ -41,6 +41,15 @@ constexpr int kBX = 64, kBY = 4, kNY = 8, kTH = kBY * kNY;  // 64 x 32 tile, 256
 // stencil reads the inner ring only.  72 x 40 boxes keep every TMA row a
 // multiple of 16 B for fp32 and fp64.
 constexpr int kHalo = 4;
+#ifndef SG_HINT_FIELD
+#define SG_HINT_FIELD 0
+#endif
+#ifndef SG_HINT_HIST
+#define SG_HINT_HIST 0
+#endif
+#ifndef SG_STCS
+#define SG_STCS 0
+#endif
 #ifndef SG_FP32_MINB
 #define SG_FP32_MINB 3
 #endif
@@ -50,7 +59,7 @@ struct StepArgs {
   // TMA descriptors (3-D views {ldx, rows, planes}; see sg_prop.cu tmap_*)
   CUtensorMap f_halo[2];  // field buffers, box = halo'd tile (load)
   CUtensorMap f_tile[2];  // field buffers, box = tile (store)
-  CUtensorMap s_tile;     // state buffer (inc / w), box = tile (load + store)
+  CUtensorMap s_tile;     // state buffer (inc / w, updated in place), box = tile
   CUtensorMap h_tile;     // history buffer {ldx, nzp, shots*steps}, box = tile
   T* f[2];                // field buffers (row 0, col 0, shot 0)
   T* state;               // inc (forward) / w (adjoint), updated in place
@@ -136,6 +145,21 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+// L2 eviction-priority policies (the encodings CUTLASS uses for
+// CacheHintSm90::EVICT_FIRST / EVICT_LAST)
+constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
+constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
+
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map,
+                                                 uint64_t* bar, int x, int y, int z,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "l"(policy)
       : "memory");
 }
 
@@ -302,11 +326,25 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
         (SM::SW * SM::SH + (LOAD_HIST ? 2 : 1) * SM::TILE) * (uint32_t)sizeof(T);
     mbar_expect_tx(&bar[s], bytes);
     // rows of a guarded plane: data row i lives at plane row kGuard + i
+    // the working set (fields, state) is kept in L2; the history stream,
+    // read once, is evicted first so it does not push the working set out
+#if SG_HINT_FIELD
+    tma_load_3d_hint(st, &a.f_halo[a.cur], &bar[s], j0 - kHalo, kGuard + i0 - kHalo, b,
+                     kEvictLast);
+    tma_load_3d_hint(st + SM::HALO, &a.s_tile, &bar[s], j0, kGuard + i0, b, kEvictLast);
+#else
     tma_load_3d(st, &a.f_halo[a.cur], &bar[s], j0 - kHalo, kGuard + i0 - kHalo, b);
     tma_load_3d(st + SM::HALO, &a.s_tile, &bar[s], j0, kGuard + i0, b);
-    if (LOAD_HIST)
+#endif
+    if (LOAD_HIST) {
+#if SG_HINT_HIST
+      tma_load_3d_hint(st + SM::HALO + SM::TILE, &a.h_tile, &bar[s], j0, i0,
+                       b * a.hist_steps + a.hist_slot, kEvictFirst);
+#else
       tma_load_3d(st + SM::HALO + SM::TILE, &a.h_tile, &bar[s], j0, i0,
                   b * a.hist_steps + a.hist_slot);
+#endif
+    }
   };
   if (tid == 0) issue(0);
 
@@ -411,7 +449,11 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
                 if (r == i && c == j) acc += a.amp * a.src_w[b * 4 + t] * im[qq];
               }
             }
-            if (HIST) hout[qq * ldx] = acc;
+  #if SG_STCS
+          if (HIST) __stcs(hout + qq * ldx, acc);  // streaming store: evict first
+#else
+          if (HIST) hout[qq * ldx] = acc;
+#endif
             const T so = dd[qq] * (sv + a.dt2 * acc);
             sout[qq * ldx] = so;
             fout[qq * ldx] = dd[qq] * ucs[h] + so;

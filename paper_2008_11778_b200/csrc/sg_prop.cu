@@ -24,6 +24,7 @@
 #include "seisgpu.h"
 #include "sg_common.cuh"
 #include "sg_kernels.cuh"
+#include "sg_kernels2.cuh"
 
 namespace sg {
 thread_local std::string g_err;
@@ -253,8 +254,12 @@ struct sg_handle {
   int* bsrc_rc = nullptr;
   void* bsrc_w = nullptr;
   std::map<std::string, CUtensorMap> tmaps;  // TMA descriptors by buffer/kind
-  void *u0 = nullptr, *u1 = nullptr, *inc = nullptr;
-  void *l0 = nullptr, *l1 = nullptr, *w = nullptr;
+  void *u0 = nullptr, *u1 = nullptr, *inc = nullptr, *inc2 = nullptr;  // fields, states
+  void *l0 = nullptr, *l1 = nullptr, *w = nullptr, *w2 = nullptr;
+  // receivers grouped by the tile holding their first tap (two-step kernel)
+  int* tile_rec_ptr = nullptr;
+  int* tile_rec = nullptr;
+  int* rec_rc = nullptr;
   void* gath = nullptr;
   void* hist = nullptr;
   void* ckpt = nullptr;
@@ -312,8 +317,8 @@ void drop_graphs(sg_handle* h) {
 void free_batch(sg_handle* h) {
   drop_graphs(h);
   h->tmaps.clear();
-  void** bufs[] = {(void**)&h->bsrc_rc, &h->bsrc_w, &h->u0, &h->u1, &h->inc, &h->l0, &h->l1,
-                   &h->w, &h->gath, &h->hist, &h->ckpt, &h->img, &h->acc_img,
+  void** bufs[] = {(void**)&h->bsrc_rc, &h->bsrc_w, &h->u0, &h->u1, &h->inc, &h->inc2, &h->l0,
+                   &h->l1, &h->w, &h->w2, &h->gath, &h->hist, &h->ckpt, &h->img, &h->acc_img,
                    (void**)&h->part, (void**)&h->scal};
   for (auto p : bufs) dfree(p);
   h->B = 0;
@@ -322,7 +327,7 @@ void free_batch(sg_handle* h) {
 // bytes per shot for the batch buffers in a given reconstruction mode
 double per_shot_bytes(const sg_handle* h, int recon, int K, int ncp) {
   const double e = h->esz;
-  double b = 6.0 * h->plane + (double)h->d.nt * h->d.n_rec + h->hplane;
+  double b = 8.0 * h->plane + (double)h->d.nt * h->d.n_rec + h->hplane;
   if (recon == SG_RECON_FULL) b += (double)h->d.nt * h->hplane;
   else b += (double)K * h->hplane + 2.0 * ncp * h->plane;
   return b * e + 64.0;
@@ -337,6 +342,7 @@ int ensure_batch(sg_handle* h) {
   budget -= 4.0 * (h->plane + h->ldx + h->tail) * h->esz + (64 << 20);  // statics + slack
   int K = h->d.checkpoint_every > 0 ? h->d.checkpoint_every
                                     : std::max(1, (int)std::ceil(std::sqrt((double)nt)));
+  if (h->d.checkpoint_every <= 0) K += K & 1;  // even: same launch pairing as FULL
   K = std::min(K, nt);
   const int ncp = (nt + K - 1) / K;
   const int want = h->d.batch > 0 ? std::min(h->d.batch, h->d.n_shots) : h->d.n_shots;
@@ -362,9 +368,11 @@ int ensure_batch(sg_handle* h) {
   SG_TRY(dalloc(h, &h->u0, fb));
   SG_TRY(dalloc(h, &h->u1, fb));
   SG_TRY(dalloc(h, &h->inc, fb));
+  SG_TRY(dalloc(h, &h->inc2, fb));
   SG_TRY(dalloc(h, &h->l0, fb));
   SG_TRY(dalloc(h, &h->l1, fb));
   SG_TRY(dalloc(h, &h->w, fb));
+  SG_TRY(dalloc(h, &h->w2, fb));
   SG_TRY(dalloc(h, &h->gath, (size_t)B * nt * h->d.n_rec * e));
   SG_TRY(dalloc(h, &h->hist, (size_t)B * h->hist_steps * h->hplane * e));
   if (recon == SG_RECON_CHECKPOINT)
@@ -417,7 +425,7 @@ int ngroups(const sg_handle* h, int count) {
 // TMA descriptors.  Guarded buffers (fields, state) are viewed as 3-D
 // {ldx, nzp + 2 kGuard, B} starting after the lead row; histories as
 // {ldx, nzp, planes}.  Out-of-bounds boxes read as zero and are clipped on store.
-enum MapKind { MAP_HALO = 0, MAP_TILE = 1, MAP_HIST = 2 };
+enum MapKind { MAP_HALO = 0, MAP_TILE = 1, MAP_HIST = 2, MAP_HALO2 = 3, MAP_RING = 4 };
 
 template <typename T, int R>
 int get_map(sg_handle* h, void* base, int kind, int64_t planes, CUtensorMap* out) {
@@ -436,8 +444,15 @@ int get_map(sg_handle* h, void* base, int kind, int64_t planes, CUtensorMap* out
   void* g = (kind == MAP_HIST) ? base : (void*)((char*)base + (size_t)h->ldx * sizeof(T));
   cuuint64_t dims[3] = {(cuuint64_t)h->ldx, (cuuint64_t)rows, (cuuint64_t)planes};
   cuuint64_t strides[2] = {(cuuint64_t)h->ldx * sizeof(T), (cuuint64_t)pl * sizeof(T)};
-  cuuint32_t box[3] = {(cuuint32_t)(kind == MAP_HALO ? BX + 2 * kHalo : BX),
-                       (cuuint32_t)(kind == MAP_HALO ? TH + 2 * kHalo : TH), 1};
+  cuuint32_t bw = BX, bh = TH;
+  if (kind == MAP_HALO || kind == MAP_RING) {
+    bw = BX + 2 * kHalo;
+    bh = TH + 2 * kHalo;
+  } else if (kind == MAP_HALO2) {
+    bw = kUW;
+    bh = kUH;
+  }
+  cuuint32_t box[3] = {bw, bh, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUtensorMap m;
   CUresult r = enc(&m, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
@@ -452,26 +467,27 @@ int get_map(sg_handle* h, void* base, int kind, int64_t planes, CUtensorMap* out
 }
 
 template <typename T, int R>
-int step_maps(sg_handle* h, StepArgs<T>& a, void* F0, void* F1, void* state, void* hist,
+int step_maps(sg_handle* h, StepArgs<T>& a, void* F0, void* F1, void* S0, void* S1, void* hist,
               int64_t hist_planes) {
   SG_TRY((get_map<T, R>(h, F0, MAP_HALO, h->B, &a.f_halo[0])));
   SG_TRY((get_map<T, R>(h, F1, MAP_HALO, h->B, &a.f_halo[1])));
   SG_TRY((get_map<T, R>(h, F0, MAP_TILE, h->B, &a.f_tile[0])));
   SG_TRY((get_map<T, R>(h, F1, MAP_TILE, h->B, &a.f_tile[1])));
-  SG_TRY((get_map<T, R>(h, state, MAP_TILE, h->B, &a.s_tile)));
+  (void)S1;  // the one-step kernel updates its state in place
+  SG_TRY((get_map<T, R>(h, S0, MAP_TILE, h->B, &a.s_tile)));
   if (hist) SG_TRY((get_map<T, R>(h, hist, MAP_HIST, hist_planes, &a.h_tile)));
   return SG_OK;
 }
 
 template <typename T>
-int step_args(sg_handle* h, StepArgs<T>& a, void* F0, void* F1, void* state, void* hist,
+int step_args(sg_handle* h, StepArgs<T>& a, void* F0, void* F1, void* S0, void* S1, void* hist,
               int64_t hist_planes) {
   std::memset(&a, 0, sizeof(a));
-  if (h->d.order == 8) SG_TRY((step_maps<T, 4>(h, a, F0, F1, state, hist, hist_planes)));
-  else SG_TRY((step_maps<T, 1>(h, a, F0, F1, state, hist, hist_planes)));
+  if (h->d.order == 8) SG_TRY((step_maps<T, 4>(h, a, F0, F1, S0, S1, hist, hist_planes)));
+  else SG_TRY((step_maps<T, 1>(h, a, F0, F1, S0, S1, hist, hist_planes)));
   a.f[0] = field<T>(F0, h);
   a.f[1] = field<T>(F1, h);
-  a.state = field<T>(state, h);
+  a.state = field<T>(S0, h);
   a.inv_m = field<T>(h->inv_m_buf, h);
   a.pz = reinterpret_cast<const T*>(h->pz_buf) + kGuard;
   a.px = reinterpret_cast<const T*>(h->px_buf) + kGuard;
@@ -575,18 +591,129 @@ struct FwdPlan {
   int64_t gsrc_shot = 0;
   int gsrc_n0 = 0;
   bool ckpt_save = false;   // save (u_n, inc_n) at n % K == 0
-  void* fu0 = nullptr;      // field buffers (default u0/u1/inc)
+  void* fu0 = nullptr;      // field / state buffers (default u0/u1, inc/inc2)
   void* fu1 = nullptr;
-  void* finc = nullptr;
+  void* fs0 = nullptr;
+  void* fs1 = nullptr;
 };
 
+// two-step (temporally blocked) kernels: fp32 only, no Born grid source, no
+// v-history.  Opt-in (desc.step_mode == 2): measured slower than the one-step
+// kernel on B200 at C3 and C5 (profiles/r01_step_kernels_by_config.txt).
+bool two_step_ok(const sg_handle* h) { return h->esz == 4 && h->d.step_mode == 2; }
+
 template <typename T>
-int enq_forward(sg_handle* h, cudaStream_t s, int count, int n0, int n1, const FwdPlan& p) {
+int step2_args(sg_handle* h, Step2Args<T>& a, void* F0, void* F1, void* S0, void* S1,
+               void* hist, int64_t hist_planes) {
+  std::memset(&a, 0, sizeof(a));
+  SG_TRY((get_map<T, 4>(h, F0, MAP_HALO2, h->B, &a.f_halo2[0])));
+  SG_TRY((get_map<T, 4>(h, F1, MAP_HALO2, h->B, &a.f_halo2[1])));
+  SG_TRY((get_map<T, 4>(h, S0, MAP_RING, h->B, &a.s_ring[0])));
+  SG_TRY((get_map<T, 4>(h, S1, MAP_RING, h->B, &a.s_ring[1])));
+  SG_TRY((get_map<T, 4>(h, h->inv_m_buf, MAP_RING, 1, &a.m_ring[0])));
+  if (hist) SG_TRY((get_map<T, 4>(h, hist, MAP_HIST, hist_planes, &a.h_tile)));
+  a.f[0] = field<T>(F0, h);
+  a.f[1] = field<T>(F1, h);
+  a.state[0] = field<T>(S0, h);
+  a.state[1] = field<T>(S1, h);
+  a.pz = reinterpret_cast<const T*>(h->pz_buf) + kGuard;
+  a.px = reinterpret_cast<const T*>(h->px_buf) + kGuard;
+  a.plane = h->plane;
+  a.nzp = h->nzp;
+  a.nxp = h->nxp;
+  a.ldx = h->ldx;
+  a.tiles_x = h->tiles_x;
+  a.ntiles = h->ntiles;
+  a.dt2 = (T)(h->d.dt * h->d.dt);
+  for (int k = 0; k < 5; ++k) {
+    a.cz[k] = (T)h->cz[k];
+    a.cx[k] = (T)h->cx[k];
+  }
+  a.hplane = h->hplane;
+  a.tile_rec_ptr = h->tile_rec_ptr;
+  a.tile_rec = h->tile_rec;
+  a.rec_rc = h->rec_rc;
+  a.rec_w = reinterpret_cast<const T*>(h->rec_w);
+  a.nrec = h->d.n_rec;
+  a.inj_row0 = h->inj_row0;
+  a.inj_nrows = h->inj_nrows;
+  a.inj_ptr = h->inj_ptr;
+  a.inj_rec = h->inj_rec;
+  a.inj_w = reinterpret_cast<const T*>(h->inj_w);
+  return SG_OK;
+}
+
+// shots per group for the two-step kernel (2 CTAs/SM)
+int group2_for(const sg_handle* h, int count) {
+  if (h->d.group > 0) return std::max(1, std::min(h->d.group, count));
+  const int slots = h->nsm * 2;
+  int best = 1;
+  double best_cost = 1e300;
+  for (int G = 1; G <= std::min(8, count); ++G) {
+    const int64_t items = (int64_t)h->ntiles * ((count + G - 1) / G);
+    const double rounds = (double)((items + slots - 1) / slots);
+    const double cost = rounds * G * (1.0 + 0.6 / G);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = G;
+    }
+  }
+  return best;
+}
+
+template <int R, bool ADJ, bool HIST, bool GATHER>
+void launch_step2_f(const sg_handle* h, cudaStream_t s, const Step2Args<float>& a) {
+  static bool attr = false;
+  constexpr int smem = step2_smem_bytes<ADJ>();
+  if (!attr) {
+    cudaFuncSetAttribute(k_step2<R, ADJ, HIST, GATHER>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  dim3 grid(h->ntiles, (a.count + a.G - 1) / a.G), block(kEW, kTY2);
+  k_step2<R, ADJ, HIST, GATHER><<<grid, block, smem, s>>>(a);
+  count_launch();
+}
+
+template <bool ADJ>
+void launch_step2(const sg_handle* h, cudaStream_t s, const Step2Args<float>& a) {
+  const bool hs = a.hist_on != 0;
+  const bool ga = !ADJ && a.gather != nullptr;
+#define L2(R)                                                           \
+  do {                                                                  \
+    if (hs && ga) launch_step2_f<R, ADJ, true, true>(h, s, a);          \
+    else if (hs) launch_step2_f<R, ADJ, true, false>(h, s, a);          \
+    else if (ga) launch_step2_f<R, ADJ, false, true>(h, s, a);          \
+    else launch_step2_f<R, ADJ, false, false>(h, s, a);                 \
+  } while (0)
+  if (h->d.order == 8) L2(4);
+  else L2(1);
+#undef L2
+}
+
+template <typename T>
+void launch_step2_t(const sg_handle* h, cudaStream_t s, const Step2Args<T>& a, bool adj) {
+  if constexpr (sizeof(T) == 4) {
+    if (adj) launch_step2<true>(h, s, a);
+    else launch_step2<false>(h, s, a);
+  }
+}
+
+// Forward steps n0 .. n1-1.  `cur` selects the input buffers (F[cur], S[cur])
+// and flips after every launch (one or two steps).
+template <typename T>
+int enq_forward(sg_handle* h, cudaStream_t s, int count, int n0, int n1, const FwdPlan& p,
+                int* curp = nullptr) {
   void* U0 = p.fu0 ? p.fu0 : h->u0;
   void* U1 = p.fu1 ? p.fu1 : h->u1;
-  void* INC = p.finc ? p.finc : h->inc;
+  const bool use2 = two_step_ok(h) && p.gsrc == nullptr;
+  void* S0 = p.fs0 ? p.fs0 : h->inc;
+  // the one-step kernel reads and writes its own cells only: state in place
+  void* S1 = use2 ? (p.fs1 ? p.fs1 : h->inc2) : S0;
+  int cur_local = 0;
+  int& cur = curp ? *curp : cur_local;
   StepArgs<T> a;
-  SG_TRY(step_args<T>(h, a, U0, U1, INC, p.hist.base, p.hist.shots * p.hist.steps));
+  SG_TRY(step_args<T>(h, a, U0, U1, S0, S1, p.hist.base, p.hist.shots * p.hist.steps));
   a.count = count;
   if (p.point) {
     a.src_rc = h->bsrc_rc;
@@ -601,20 +728,55 @@ int enq_forward(sg_handle* h, cudaStream_t s, int count, int n0, int n1, const F
   a.hist = reinterpret_cast<T*>(p.hist.base);
   a.hplane = h->hplane;
   a.gather_stride = (int64_t)h->d.nt * h->d.n_rec;
+  Step2Args<T> a2;
+  if (use2) {
+    SG_TRY(step2_args<T>(h, a2, U0, U1, S0, S1, p.hist.base, p.hist.shots * p.hist.steps));
+    a2.count = count;
+    a2.G = group2_for(h, count);
+    if (p.point) {
+      a2.src_rc = h->bsrc_rc;
+      a2.src_w = reinterpret_cast<const T*>(h->bsrc_w);
+    }
+    a2.hist_on = a.hist_on;
+    a2.hist_steps = p.hist.steps;
+    a2.hist = a.hist;
+    a2.gather = p.gathers ? reinterpret_cast<T*>(h->gath) : nullptr;
+    a2.gather_stride = a.gather_stride;
+  }
   const size_t pb = span_bytes(h, count);
   const size_t sb = span_bytes(h, h->B);
-  for (int n = n0; n < n1; ++n) {
-    a.cur = (n - n0) & 1;
+  void* F[2] = {U0, U1};
+  void* S[2] = {S0, S1};
+  int n = n0;
+  while (n < n1) {
     if (p.ckpt_save && n % h->K == 0) {
       char* slot = (char*)h->ckpt + (size_t)(n / h->K) * 2 * sb;
-      cudaMemcpyAsync(slot, a.cur ? U1 : U0, pb, cudaMemcpyDeviceToDevice, s);
-      cudaMemcpyAsync(slot + sb, INC, pb, cudaMemcpyDeviceToDevice, s);
+      cudaMemcpyAsync(slot, F[cur], pb, cudaMemcpyDeviceToDevice, s);
+      cudaMemcpyAsync(slot + sb, S[cur], pb, cudaMemcpyDeviceToDevice, s);
     }
-    a.amp = (T)h->wavelet[n];
-    if (a.hist_on) a.hist_slot = p.hist.slot(n);
-    if (p.gsrc) a.gsrc = reinterpret_cast<const T*>(p.gsrc) + (int64_t)(n - p.gsrc_n0) * h->hplane;
-    a.gather = p.gathers ? reinterpret_cast<T*>(h->gath) + (int64_t)n * h->d.n_rec : nullptr;
-    launch_step<T, false>(h, s, a);
+    const bool two = use2 && n + 1 < n1 && !(p.ckpt_save && (n + 1) % h->K == 0);
+    if (two) {
+      a2.cur = cur;
+      a2.n0 = n;
+      a2.amp0 = (T)h->wavelet[n];
+      a2.amp1 = (T)h->wavelet[n + 1];
+      if (a2.hist_on) {
+        a2.slot0 = p.hist.slot(n);
+        a2.slot1 = p.hist.slot(n + 1);
+      }
+      launch_step2_t<T>(h, s, a2, false);
+      n += 2;
+    } else {
+      a.cur = cur;
+      a.amp = (T)h->wavelet[n];
+      if (a.hist_on) a.hist_slot = p.hist.slot(n);
+      if (p.gsrc)
+        a.gsrc = reinterpret_cast<const T*>(p.gsrc) + (int64_t)(n - p.gsrc_n0) * h->hplane;
+      a.gather = p.gathers ? reinterpret_cast<T*>(h->gath) + (int64_t)n * h->d.n_rec : nullptr;
+      launch_step<T, false>(h, s, a);
+      n += 1;
+    }
+    cur ^= 1;
   }
   return SG_OK;
 }
@@ -625,11 +787,17 @@ struct AdjPlan {
   void* vhist = nullptr;       // optional v store (nt planes, compact rows)
 };
 
-// adjoint steps n = n_hi-1 .. n_lo; state V in l0/l1 (parity from n), w in place
+// Adjoint steps n = n_hi-1 .. n_lo (descending); fields V in l0/l1, states w/w2;
+// `cur` flips after every launch and continues across calls of one sweep.
 template <typename T>
-int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, const AdjPlan& p) {
+int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, const AdjPlan& p,
+                int* curp = nullptr) {
+  int cur_local = 0;
+  int& cur = curp ? *curp : cur_local;
+  const bool use2 = two_step_ok(h) && p.vhist == nullptr;
+  void* W1 = use2 ? h->w2 : h->w;  // one-step kernel: state in place
   StepArgs<T> a;
-  SG_TRY(step_args<T>(h, a, h->l0, h->l1, h->w, p.hist.base, p.hist.shots * p.hist.steps));
+  SG_TRY(step_args<T>(h, a, h->l0, h->l1, h->w, W1, p.hist.base, p.hist.shots * p.hist.steps));
   a.count = count;
   a.ybar_stride = (int64_t)h->d.nt * h->d.n_rec;
   a.hist_on = p.hist.base != nullptr;
@@ -637,13 +805,40 @@ int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, con
   a.image = a.hist_on ? reinterpret_cast<T*>(h->img) : nullptr;
   a.image_stride = h->hplane;
   a.vhist_stride = (int64_t)h->d.nt * h->hplane;
-  const int nt = h->d.nt;
-  for (int n = n_hi - 1; n >= n_lo; --n) {
-    a.cur = (nt - 1 - n) & 1;
-    a.ybar = p.inject ? reinterpret_cast<const T*>(h->gath) + (int64_t)n * h->d.n_rec : nullptr;
-    if (a.hist_on) a.hist_slot = p.hist.slot(n);
-    a.vhist = p.vhist ? reinterpret_cast<T*>(p.vhist) + (int64_t)n * h->hplane : nullptr;
-    launch_step<T, true>(h, s, a);
+  Step2Args<T> a2;
+  if (use2) {
+    SG_TRY(step2_args<T>(h, a2, h->l0, h->l1, h->w, h->w2, p.hist.base,
+                         p.hist.shots * p.hist.steps));
+    a2.count = count;
+    a2.G = group2_for(h, count);
+    a2.ybar_stride = a.ybar_stride;
+    a2.hist_on = a.hist_on;
+    a2.hist_steps = p.hist.steps;
+    a2.image = a.image;
+    a2.image_stride = a.image_stride;
+  }
+  int n = n_hi - 1;
+  while (n >= n_lo) {
+    const T* yb = p.inject ? reinterpret_cast<const T*>(h->gath) + (int64_t)n * h->d.n_rec : nullptr;
+    if (use2 && n - 1 >= n_lo) {
+      a2.cur = cur;
+      a2.n0 = n;
+      a2.ybar = yb;
+      if (a2.hist_on) {
+        a2.slot0 = p.hist.slot(n);
+        a2.slot1 = p.hist.slot(n - 1);
+      }
+      launch_step2_t<T>(h, s, a2, true);
+      n -= 2;
+    } else {
+      a.cur = cur;
+      a.ybar = yb;
+      if (a.hist_on) a.hist_slot = p.hist.slot(n);
+      a.vhist = p.vhist ? reinterpret_cast<T*>(p.vhist) + (int64_t)n * h->hplane : nullptr;
+      launch_step<T, true>(h, s, a);
+      n -= 1;
+    }
+    cur ^= 1;
   }
   return SG_OK;
 }
@@ -728,11 +923,13 @@ int zero_fields(sg_handle* h, bool fwd, bool adj, int cnt) {
     SG_CK(cudaMemsetAsync(h->u0, 0, b, h->stream));
     SG_CK(cudaMemsetAsync(h->u1, 0, b, h->stream));
     SG_CK(cudaMemsetAsync(h->inc, 0, b, h->stream));
+    SG_CK(cudaMemsetAsync(h->inc2, 0, b, h->stream));
   }
   if (adj) {
     SG_CK(cudaMemsetAsync(h->l0, 0, b, h->stream));
     SG_CK(cudaMemsetAsync(h->l1, 0, b, h->stream));
     SG_CK(cudaMemsetAsync(h->w, 0, b, h->stream));
+    SG_CK(cudaMemsetAsync(h->w2, 0, b, h->stream));
   }
   return SG_OK;
 }
@@ -840,6 +1037,7 @@ int do_adjoint_batch(sg_handle* h, int cnt, const void* cached_hist, int64_t cac
   SG_TRY(run_graph(h, "adj_ckpt/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
     const size_t pb = span_bytes(h, cnt);
     const size_t sb = span_bytes(h, h->B);
+    int acur = 0;  // adjoint ping-pong position, continues across segments
     for (int seg = h->ncp - 1; seg >= 0; --seg) {
       const int n0 = seg * h->K;
       const int n1 = std::min(nt, n0 + h->K);
@@ -852,7 +1050,7 @@ int do_adjoint_batch(sg_handle* h, int cnt, const void* cached_hist, int64_t cac
       SG_TRY(enq_forward<T>(h, s, cnt, n0, n1, fp));
       AdjPlan ap;
       ap.hist = main_hist(h, n0);
-      SG_TRY(enq_adjoint<T>(h, s, cnt, n1, n0, ap));
+      SG_TRY(enq_adjoint<T>(h, s, cnt, n1, n0, ap, &acur));
     }
     return SG_OK;
   }));
@@ -1007,23 +1205,22 @@ int born_forward_t(sg_handle* h, int shot0, int count, const void* m_r, void* ou
       SG_TRY(load_batch_sources(h, b0, cnt));
       SG_TRY(zero_fields(h, true, true, cnt));
       SG_TRY(run_graph(h, "born_fwd_lock/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
+        int cb = 0, cs = 0;  // ping-pong positions of the background / scattered fields
         for (int n = 0; n < nt; ++n) {
           FwdPlan bg;
           bg.gathers = false;
           bg.hist = main_hist(h, n);
-          // alternate the background ping-pong by running one step at a time
-          bg.fu0 = (n & 1) ? h->u1 : h->u0;
-          bg.fu1 = (n & 1) ? h->u0 : h->u1;
-          SG_TRY(enq_forward<T>(h, s, cnt, n, n + 1, bg));
+          SG_TRY(enq_forward<T>(h, s, cnt, n, n + 1, bg, &cb));
           FwdPlan sc;
           sc.point = false;
           sc.gsrc = h->hist;
           sc.gsrc_shot = (int64_t)h->hist_steps * h->hplane;
           sc.gsrc_n0 = n;
-          sc.fu0 = (n & 1) ? h->l1 : h->l0;
-          sc.fu1 = (n & 1) ? h->l0 : h->l1;
-          sc.finc = h->w;
-          SG_TRY(enq_forward<T>(h, s, cnt, n, n + 1, sc));
+          sc.fu0 = h->l0;
+          sc.fu1 = h->l1;
+          sc.fs0 = h->w;
+          sc.fs1 = h->w2;
+          SG_TRY(enq_forward<T>(h, s, cnt, n, n + 1, sc, &cs));
         }
         return SG_OK;
       }));
@@ -1152,7 +1349,22 @@ int time_kernel_t(sg_handle* h, int which, int count, int reps, float* ms) {
   SG_CK(cudaEventCreate(&e1));
   const int n = h->d.nt / 2;
   auto body = [&](cudaStream_t s) -> int {
-    if (which == 0 || which == 2) {
+    if (which == 3 || which == 4) {
+      // two-step launches (two time steps each); history rotates through the buffer
+      HistRef hr = main_hist(h, n);
+      hr.rotate = true;
+      for (int r = 0; r < reps; ++r) {
+        if (which == 3) {
+          FwdPlan p;
+          p.hist = hr;
+          SG_TRY(enq_forward<T>(h, s, count, n + 2 * (r & 1), n + 2 * (r & 1) + 2, p));
+        } else {
+          AdjPlan p;
+          p.hist = hr;
+          SG_TRY(enq_adjoint<T>(h, s, count, n + 2, n, p));
+        }
+      }
+    } else if (which == 0 || which == 2) {
       FwdPlan p;
       if (which == 0) {
         p.hist = main_hist(h, n);
@@ -1246,7 +1458,8 @@ int sg_destroy(sg_handle* h) {
   if (!h) return SG_OK;
   cudaSetDevice(h->d.device);
   free_batch(h);
-  void** bufs[] = {&h->inv_m_buf, &h->pz_buf, &h->px_buf, &h->gscale_buf, (void**)&h->src_rc,
+  void** bufs[] = {(void**)&h->rec_rc, (void**)&h->tile_rec_ptr, (void**)&h->tile_rec,
+                   &h->inv_m_buf, &h->pz_buf, &h->px_buf, &h->gscale_buf, (void**)&h->src_rc,
                    &h->src_w, (void**)&h->rec_ij, &h->rec_w, (void**)&h->inj_ptr,
                    (void**)&h->inj_rec, &h->inj_w, &h->born_hist};
   for (auto p : bufs) dfree(p);
@@ -1326,9 +1539,30 @@ int sg_set_geometry(sg_handle* h, const int32_t* src_rows, const int32_t* src_co
     irec[at] = e % R;
     iw[at] = rec_w[e];
   }
+  // receivers grouped by the tile of their first tap (two-step forward)
+  std::vector<int> rrc(8 * R), tcount(h->ntiles + 1, 0), trec(R);
+  for (int e = 0; e < 4 * R; ++e) {
+    rrc[2 * e] = rec_rows[e];
+    rrc[2 * e + 1] = rec_cols[e];
+  }
+  auto tile_of = [&](int r) { return (rec_rows[r] / TH) * h->tiles_x + rec_cols[r] / BX; };
+  for (int r = 0; r < R; ++r) tcount[tile_of(r) + 1]++;
+  for (int t = 0; t < h->ntiles; ++t) tcount[t + 1] += tcount[t];
+  {
+    std::vector<int> fill(tcount.begin(), tcount.end() - 1);
+    for (int r = 0; r < R; ++r) trec[fill[tile_of(r)]++] = r;
+  }
   void** bufs[] = {(void**)&h->src_rc, &h->src_w, (void**)&h->rec_ij, &h->rec_w,
-                   (void**)&h->inj_ptr, (void**)&h->inj_rec, &h->inj_w};
+                   (void**)&h->inj_ptr, (void**)&h->inj_rec, &h->inj_w,
+                   (void**)&h->rec_rc, (void**)&h->tile_rec_ptr, (void**)&h->tile_rec};
   for (auto p : bufs) dfree(p);
+  SG_TRY(dalloc(h, (void**)&h->rec_rc, rrc.size() * sizeof(int)));
+  SG_CK(cudaMemcpy(h->rec_rc, rrc.data(), rrc.size() * sizeof(int), cudaMemcpyHostToDevice));
+  SG_TRY(dalloc(h, (void**)&h->tile_rec_ptr, tcount.size() * sizeof(int)));
+  SG_CK(cudaMemcpy(h->tile_rec_ptr, tcount.data(), tcount.size() * sizeof(int),
+                   cudaMemcpyHostToDevice));
+  SG_TRY(dalloc(h, (void**)&h->tile_rec, trec.size() * sizeof(int)));
+  SG_CK(cudaMemcpy(h->tile_rec, trec.data(), trec.size() * sizeof(int), cudaMemcpyHostToDevice));
   SG_TRY(dalloc(h, (void**)&h->src_rc, src.size() * sizeof(int)));
   SG_CK(cudaMemcpy(h->src_rc, src.data(), src.size() * sizeof(int), cudaMemcpyHostToDevice));
   SG_TRY(dalloc(h, (void**)&h->rec_ij, rij.size() * sizeof(int)));

@@ -131,7 +131,7 @@ class Propagator:
 
     def __init__(self, grid, geometry, wavelet, config=SimConfig(), dtype="float64",
                  device=None, recon="auto", batch=0, checkpoint_every=0, use_graphs=True,
-                 mem_budget_bytes=0.0, group=0):
+                 mem_budget_bytes=0.0, group=0, step_mode=0):
         torch = _torch()
         self.lib = _lib.load()
         if not torch.cuda.is_available():
@@ -160,6 +160,7 @@ class Propagator:
         d.device = self.device.index
         d.use_graphs = 1 if use_graphs else 0
         d.group = int(group)
+        d.step_mode = int(step_mode)
         d.dx, d.dz, d.dt = grid.dx, grid.dz, geometry.dt
         d.cfl_safety = config.cfl_safety
         d.mem_budget_bytes = float(mem_budget_bytes)
