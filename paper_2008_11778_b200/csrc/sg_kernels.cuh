@@ -119,6 +119,14 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Programmatic dependent launch: let the next kernel in the stream start its
+// prologue once every CTA of this grid is resident, and wait for the previous
+// grid's completion (and memory) before touching data it produced or reads.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
@@ -288,6 +296,8 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
 
   if constexpr (!ADJ && (FL & FL_GATHER) != 0) {
     if ((int)blockIdx.x >= a.ntiles) {
+      pdl_wait();
+      pdl_launch_dependents();
       // receiver sampling for this group's shots: gather[n, r] = sum_k w_k u_n[tap_k]
       // (seisopt/wavesim.py:225-226, sampled before the update, :287)
       const T* __restrict__ u = a.f[a.cur];
@@ -346,8 +356,6 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
 #endif
     }
   };
-  if (tid == 0) issue(0);
-
   const int j = j0 + threadIdx.x;
   const bool vj = j < a.nxp;
   const int rb = threadIdx.y * kNY;  // first tile row owned by this thread
@@ -360,6 +368,10 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
   // accumulator starts from the stored image (prefetched, lands during shot 0)
   T im[kNY], dd[kNY], img[kNY];
   const T pxj = vj ? a.px[j] : T(0);
+  // Prologue (may overlap the previous step under PDL): model data and the
+  // image accumulator of this launch's parity, last written two launches ago
+  // (complete: the previous grid signalled its dependents only after its own
+  // griddepcontrol.wait).
   T* ig = nullptr;
   if (LOAD_HIST) ig = a.image + (int64_t)grp * a.image_stride + o0;
 #pragma unroll
@@ -374,6 +386,10 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
       img[q] = T(0);
     }
   }
+  // everything below reads or writes fields/states of the previous step
+  pdl_wait();
+  pdl_launch_dependents();
+  if (tid == 0) issue(0);
 
   for (int k = 0; k < nb; ++k) {
     const int b = b0 + k;

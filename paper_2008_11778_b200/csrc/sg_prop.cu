@@ -251,6 +251,7 @@ struct sg_handle {
   int64_t hist_steps = 0; // steps of history held per shot
   int G = 0;              // set once batch buffers exist; see group_for()
   int nsm = 148;          // SMs of the device
+  bool pdl = true;        // programmatic dependent launch between step kernels
   int* bsrc_rc = nullptr;
   void* bsrc_w = nullptr;
   std::map<std::string, CUtensorMap> tmaps;  // TMA descriptors by buffer/kind
@@ -327,7 +328,7 @@ void free_batch(sg_handle* h) {
 // bytes per shot for the batch buffers in a given reconstruction mode
 double per_shot_bytes(const sg_handle* h, int recon, int K, int ncp) {
   const double e = h->esz;
-  double b = 8.0 * h->plane + (double)h->d.nt * h->d.n_rec + h->hplane;
+  double b = 8.0 * h->plane + (double)h->d.nt * h->d.n_rec + 2.0 * h->hplane;
   if (recon == SG_RECON_FULL) b += (double)h->d.nt * h->hplane;
   else b += (double)K * h->hplane + 2.0 * ncp * h->plane;
   return b * e + 64.0;
@@ -377,7 +378,7 @@ int ensure_batch(sg_handle* h) {
   SG_TRY(dalloc(h, &h->hist, (size_t)B * h->hist_steps * h->hplane * e));
   if (recon == SG_RECON_CHECKPOINT)
     SG_TRY(dalloc(h, &h->ckpt, (size_t)ncp * 2 * span_bytes(h, B)));
-  SG_TRY(dalloc(h, &h->img, (size_t)B * h->hplane * e));
+  SG_TRY(dalloc(h, &h->img, (size_t)2 * B * h->hplane * e));  // two launch-parity sets
   SG_TRY(dalloc(h, &h->acc_img, (size_t)h->hplane * e));
   h->npart = 1184;
   SG_TRY(dalloc(h, (void**)&h->part, (size_t)h->npart * 2 * sizeof(double)));
@@ -528,8 +529,19 @@ void launch_step_f(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a0) {
   a.G = group_for(h, a.count);
   a.rec_blocks = (a.G * h->d.n_rec + RB - 1) / RB;
   const int extra = (!ADJ && (FL & FL_GATHER)) ? a.rec_blocks : 0;
-  dim3 grid(h->ntiles + extra, ngroups(h, a.count)), block(kBX, kBY);
-  k_step<T, R, ADJ, FL><<<grid, block, smem, s>>>(a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(h->ntiles + extra, ngroups(h, a.count));
+  cfg.blockDim = dim3(kBX, kBY);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr_pdl[1];
+  attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  if (h->pdl) {
+    cfg.attrs = attr_pdl;
+    cfg.numAttrs = 1;
+  }
+  cudaLaunchKernelEx(&cfg, k_step<T, R, ADJ, FL>, a);
   count_launch();
 }
 
@@ -833,6 +845,8 @@ int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, con
     } else {
       a.cur = cur;
       a.ybar = yb;
+      // image accumulator set of this launch's parity (PDL-safe, see k_step)
+      if (a.hist_on) a.image = reinterpret_cast<T*>(h->img) + (int64_t)cur * h->B * h->hplane;
       if (a.hist_on) a.hist_slot = p.hist.slot(n);
       a.vhist = p.vhist ? reinterpret_cast<T*>(p.vhist) + (int64_t)n * h->hplane : nullptr;
       launch_step<T, true>(h, s, a);
@@ -952,7 +966,7 @@ template <typename T>
 int reduce_images(sg_handle* h, int cnt) {
   dim3 grid(cdiv(h->nxp, 128), h->nzp);
   k_reduce_images<T><<<grid, 128, 0, h->stream>>>(
-      reinterpret_cast<const T*>(h->img), reinterpret_cast<T*>(h->acc_img), ngroups(h, cnt), h->hplane,
+      reinterpret_cast<const T*>(h->img), reinterpret_cast<T*>(h->acc_img), 2 * h->B, h->hplane,
       h->nzp, h->nxp, h->ldx);
   count_launch();
   SG_CK(cudaGetLastError());
@@ -1013,7 +1027,7 @@ int do_forward_batch(sg_handle* h, int b0, int cnt, bool store_full_hist_ckpt_mo
 template <typename T>
 int do_adjoint_batch(sg_handle* h, int cnt, const void* cached_hist, int64_t cached_shots) {
   SG_TRY(zero_fields(h, false, true, cnt));
-  SG_CK(cudaMemsetAsync(h->img, 0, (size_t)cnt * h->hplane * h->esz, h->stream));
+  SG_CK(cudaMemsetAsync(h->img, 0, (size_t)2 * h->B * h->hplane * h->esz, h->stream));
   const int nt = h->d.nt;
   if (cached_hist != nullptr || h->recon == SG_RECON_FULL) {
     HistRef hr = main_hist(h, 0);
@@ -1434,6 +1448,10 @@ int sg_create(const sg_desc* d, sg_handle** out) {
   h->ntiles = h->tiles_x * ((h->nzp + TH - 1) / TH);
   h->rec_blocks = (d->n_rec + RB - 1) / RB;
   cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, d->device);
+  {
+    const char* e = getenv("SG_PDL");
+    h->pdl = !(e && atoi(e) == 0);
+  }
   const double rz = 1.0 / (d->dz * d->dz), rx = 1.0 / (d->dx * d->dx);
   if (d->order == 2) {
     h->cz[1] = rz;
