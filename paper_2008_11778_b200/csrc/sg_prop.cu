@@ -1219,17 +1219,22 @@ int born_forward_t(sg_handle* h, int shot0, int count, const void* m_r, void* ou
       SG_TRY(load_batch_sources(h, b0, cnt));
       SG_TRY(zero_fields(h, true, true, cnt));
       SG_TRY(run_graph(h, "born_fwd_lock/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
+        // The background keeps its whole history (FULL) or its checkpoints
+        // (CHECKPOINT) for a following LSRTM adjoint, which then needs no
+        // background re-run (4 stencil sweeps per LSRTM gradient).
+        const bool full = h->recon == SG_RECON_FULL;
         int cb = 0, cs = 0;  // ping-pong positions of the background / scattered fields
         for (int n = 0; n < nt; ++n) {
           FwdPlan bg;
           bg.gathers = false;
-          bg.hist = main_hist(h, n);
+          bg.hist = main_hist(h, full ? 0 : n);
+          bg.ckpt_save = !full;
           SG_TRY(enq_forward<T>(h, s, cnt, n, n + 1, bg, &cb));
           FwdPlan sc;
           sc.point = false;
           sc.gsrc = h->hist;
           sc.gsrc_shot = (int64_t)h->hist_steps * h->hplane;
-          sc.gsrc_n0 = n;
+          sc.gsrc_n0 = full ? 0 : n;
           sc.fu0 = h->l0;
           sc.fu1 = h->l1;
           sc.fs0 = h->w;
@@ -1267,6 +1272,10 @@ int born_adjoint_core(sg_handle* h, int shot0, int count, const void* data, int 
     if (born_cached_covers(h, b0, cnt)) {
       const void* base = (char*)h->born_hist + (size_t)(b0 - h->born_b0) * nt * h->hplane * h->esz;
       SG_TRY(do_adjoint_batch<T>(h, cnt, base, h->born_count - (b0 - h->born_b0)));
+    } else if (mode_resid == 1) {
+      // the lock-step Born forward of this batch left the background history
+      // (FULL) or its checkpoints (CHECKPOINT) in place
+      SG_TRY(do_adjoint_batch<T>(h, cnt, nullptr, 0));
     } else if (h->recon == SG_RECON_FULL) {
       // recompute and store the background history, then image against it
       SG_TRY(load_batch_sources(h, b0, cnt));
