@@ -64,16 +64,21 @@ struct Vec<double> {
 
 // fused push: f_k = g - p; df = f_k - f_prev; dg = g - g_prev; store df, dg
 // into slot `snew`; f_prev <- f_k, g_prev <- g; partial dots
-//   [0..nw)        <df, DF_i>
-//   nw             <df, df>
-//   [nw+1..2nw+1)  <f_k, DF_i>
-//   2nw+1          <f_k, df>
-//   2nw+2          <f_k, f_k>
+//   [0..nw)   <df, DF_i>
+//   nw        <df, df>
+//   nw + 1    <f_k, df>
+//   nw + 2    <f_k, f_k>
+// The projections <f_k, DF_i> of the surviving columns follow on the host
+// from <f_{k-1}, DF_i> + <df, DF_i>, so one accumulator per column suffices.
 // first != 0: only f_prev/g_prev are written and <f_k, f_k> reduced.
 // Element k of the vectorised loop covers elements [k*W, k*W + W); the tail
 // n % W (and every element when VEC is false) runs the scalar loop.
+#ifndef SG_AA_MINB
+#define SG_AA_MINB 4
+#endif
+
 template <typename T, int MW, bool VEC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, SG_AA_MINB)
     k_aa_push(const T* __restrict__ p, const T* __restrict__ g, T* __restrict__ fprev,
               T* __restrict__ gprev, T* __restrict__ DF, T* __restrict__ DG, int64_t n,
               int64_t ld, const Slots slots, int nw, int snew, int first,
@@ -81,9 +86,9 @@ __global__ void __launch_bounds__(kThreads)
   using VT = Vec<T>;
   using V = typename VT::type;
   constexpr int W = VEC ? VT::W : 1;
-  double a_dd[MW], a_fd[MW];
+  double a_dd[MW];
 #pragma unroll
-  for (int i = 0; i < MW; ++i) a_dd[i] = a_fd[i] = 0.0;
+  for (int i = 0; i < MW; ++i) a_dd[i] = 0.0;
   double dd = 0.0, fd = 0.0, ff = 0.0;
   T* dfn = DF + (int64_t)snew * ld;
   T* dgn = DG + (int64_t)snew * ld;
@@ -127,11 +132,8 @@ __global__ void __launch_bounds__(kThreads)
         if (i < nw) {
           const V c = reinterpret_cast<const V*>(DF + (int64_t)slots.s[i] * ld)[e];
 #pragma unroll
-          for (int l = 0; l < W; ++l) {
-            const double cv = (double)VT::get(c, l);
-            a_dd[i] += (double)VT::get(dfv, l) * cv;
-            a_fd[i] += (double)VT::get(fkv, l) * cv;
-          }
+          for (int l = 0; l < W; ++l)
+            a_dd[i] += (double)VT::get(dfv, l) * (double)VT::get(c, l);
         }
       }
     }
@@ -150,14 +152,12 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int i = 0; i < MW; ++i) {
       if (i < nw) {
-        const double c = (double)DF[(int64_t)slots.s[i] * ld + e];
-        a_dd[i] += (double)df * c;
-        a_fd[i] += (double)fk * c;
+        a_dd[i] += (double)df * (double)DF[(int64_t)slots.s[i] * ld + e];
       }
     }
   }
-  // block reduction of 2*nw + 3 accumulators, written as this block's partials
-  const int na = 2 * nw + 3;
+  // block reduction of nw + 3 accumulators, written as this block's partials
+  const int na = nw + 3;
   __shared__ double red[kThreads / 32][2 * kMaxMem + 3];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   auto warp_put = [&](int idx, double v) {
@@ -166,15 +166,11 @@ __global__ void __launch_bounds__(kThreads)
     if (lane == 0) red[wid][idx] = v;
   };
 #pragma unroll
-  for (int i = 0; i < MW; ++i) {
-    if (i < nw) {
-      warp_put(i, a_dd[i]);
-      warp_put(nw + 1 + i, a_fd[i]);
-    }
-  }
+  for (int i = 0; i < MW; ++i)
+    if (i < nw) warp_put(i, a_dd[i]);
   warp_put(nw, dd);
-  warp_put(2 * nw + 1, fd);
-  warp_put(2 * nw + 2, ff);
+  warp_put(nw + 1, fd);
+  warp_put(nw + 2, ff);
   __syncthreads();
   for (int k = threadIdx.x; k < na; k += blockDim.x) {
     double s = 0.0;
@@ -518,7 +514,7 @@ int push_t(sg_aa* a, const void* p, const void* g) {
     snew = slot_of(a, nw);
   }
   const int nb = grid_for(a->n);
-  const int na = first ? 3 : 2 * nw + 3;
+  const int na = nw + 3;
   T* DF = reinterpret_cast<T*>(a->DF);
   T* DG = reinterpret_cast<T*>(a->DG);
   const T* pp = reinterpret_cast<const T*>(p);
@@ -553,7 +549,7 @@ int push_t(sg_aa* a, const void* p, const void* g) {
   a->have_w = false;
   if (first) {
     // memory 0 keeps only the latest entry; otherwise this is fs[0]
-    a->fk2 = o[2];
+    a->fk2 = o[nw + 2];
     a->pushes = 1;
     a->ncols = 0;
     a->head = 0;
@@ -564,11 +560,11 @@ int push_t(sg_aa* a, const void* p, const void* g) {
   for (int i = 0; i < nw; ++i) {
     G(a, i, nw) = o[i];
     G(a, nw, i) = o[i];
-    a->bvec[i] = o[nw + 1 + i];
+    a->bvec[i] += o[i];  // <f_k, dF_i> = <f_{k-1}, dF_i> + <df, dF_i>
   }
   G(a, nw, nw) = o[nw];
-  a->bvec[nw] = o[2 * nw + 1];
-  a->fk2 = o[2 * nw + 2];
+  a->bvec[nw] = o[nw + 1];
+  a->fk2 = o[nw + 2];
   a->ncols = nw + 1;
   a->pushes += 1;
   (void)m;
