@@ -376,3 +376,66 @@ def test_lsrtm_without_cache_fp64(recon):
     # a Born forward / adjoint pair after it is unaffected
     assert rel(p.born_forward(g["m_r"]).cpu().numpy(), g["born"]) <= F64
     assert rel(p.born_adjoint(g["y"]).cpu().numpy(), g["img"]) <= F64
+
+
+def test_memory_budget_batches_and_checkpoint_fp64():
+    """A small memory budget forces several shot batches and checkpointing:
+    still the reference gradient (C1, 8th order, fp64)."""
+    _, wavesim = _api()
+    case = c1(8)
+    g = case["gold"]
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    st = oracle_setup(g["m_true"], grid, geom, cfg)
+    obs = np.stack(oracle.fwi_synthetic(st, wav.samples, geom.nt, threads=5))
+    p = wavesim.Propagator(grid, geom, wav, cfg, dtype="float64", recon="auto",
+                           mem_budget_bytes=0.1e9)
+    p.set_model(g["m_init"])
+    v, gr = p.gradient(obs)
+    q = p.query()
+    assert q["recon"] == "checkpoint" and q["batch"] < geom.n_sources
+    assert abs(v - float(g["value"])) <= F64 * float(g["value"])
+    assert rel(gr.cpu().numpy(), g["grad"]) <= F64
+
+
+@pytest.mark.parametrize("every", [37, 38, 1])
+def test_checkpoint_interval_bitwise(every):
+    """Any checkpoint interval (odd, even, 1) reproduces FULL bit for bit."""
+    _, wavesim = _api()
+    case = small_case(8, True)
+    g = case["gold"]
+    args = (case["grid"], case["geometry"], case["wavelet"], case["config"])
+    ref = wavesim.Propagator(*args, dtype="float32", recon="full")
+    ref.set_model(g["m"])
+    v0, g0 = ref.gradient(g["obs"])
+    p = wavesim.Propagator(*args, dtype="float32", recon="checkpoint", checkpoint_every=every)
+    p.set_model(g["m"])
+    v1, g1 = p.gradient(g["obs"])
+    assert v0 == v1 and torch.equal(g0, g1)
+
+
+def test_shot_ranges_sum_to_full_gradient():
+    """Gradients over shot sub-ranges (the multi-GPU shard path) add up to the
+    all-shot gradient; accumulate=True adds into the output."""
+    _, wavesim = _api()
+    case = c1(8)
+    g = case["gold"]
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    st = oracle_setup(g["m_true"], grid, geom, cfg)
+    obs = np.stack(oracle.fwi_synthetic(st, wav.samples, geom.nt, threads=5))
+    p = wavesim.Propagator(grid, geom, wav, cfg, dtype="float64")
+    p.set_model(g["m_init"])
+    va, out = p.gradient(obs[0:2], shots=(0, 2))
+    vb, out = p.gradient(obs[2:5], shots=(2, 3), out=out, accumulate=True)
+    assert abs(va + vb - float(g["value"])) <= F64 * float(g["value"])
+    assert rel(out.cpu().numpy(), g["grad"]) <= F64
+    # Born cache over several batches
+    pb = wavesim.Propagator(grid, geom, wav, cfg, dtype="float64", batch=2)
+    pb.set_model(g["m_init"])
+    pn = wavesim.Propagator(grid, geom, wav, cfg, dtype="float64")
+    pn.set_model(g["m_init"])
+    rng = np.random.default_rng(5)
+    m_r = rng.standard_normal(grid.shape) * 1e-9
+    d_ref = pn.born_forward(m_r)
+    pb.born_cache()
+    assert rel(pb.born_forward(m_r).cpu().numpy(), d_ref.cpu().numpy()) <= 1e-13
+    assert rel(pb.born_adjoint(d_ref).cpu().numpy(), pn.born_adjoint(d_ref).cpu().numpy()) <= 1e-12
