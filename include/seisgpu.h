@@ -73,7 +73,7 @@ typedef struct sg_desc {
   int32_t reserved[2];
   double dx, dz, dt;                 /* metres, seconds */
   double cfl_safety;                 /* SimConfig.cfl_safety, seisopt/wavesim.py:57 */
-  double mem_budget_bytes;           /* 0 = 90% of free device memory */
+  double mem_budget_bytes;           /* 0 = 50% of free device memory */
 } sg_desc;
 
 typedef struct sg_handle sg_handle;
@@ -144,6 +144,9 @@ int sg_fwi_gradient(sg_handle* h, int32_t shot0, int32_t count, const void* obse
  * (sg_born_cache), otherwise recomputed (lock-step forward, checkpointed
  * adjoint). */
 int sg_born_cache(sg_handle* h, int32_t shot0, int32_t count, int32_t enable);
+/* Shots whose background history is cached: a prefix of the requested range
+ * sized to the free device memory (the rest is recomputed per apply). */
+int sg_born_cached(sg_handle* h, int32_t* shot0, int32_t* count);
 int sg_born_forward(sg_handle* h, int32_t shot0, int32_t count, const void* m_r_dev,
                     void* data_dev);
 int sg_born_adjoint(sg_handle* h, int32_t shot0, int32_t count, const void* data_dev,

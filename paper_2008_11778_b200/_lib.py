@@ -71,6 +71,7 @@ SIGNATURES = {
     "sg_fwi_misfit": (C.c_int, [_P, _I32, _I32, _P, _DP]),
     "sg_fwi_gradient": (C.c_int, [_P, _I32, _I32, _P, _DP, _P, _I32]),
     "sg_born_cache": (C.c_int, [_P, _I32, _I32, _I32]),
+    "sg_born_cached": (C.c_int, [_P, _IP, _IP]),
     "sg_born_forward": (C.c_int, [_P, _I32, _I32, _P, _P]),
     "sg_born_adjoint": (C.c_int, [_P, _I32, _I32, _P, _P, _I32]),
     "sg_lsrtm_gradient": (C.c_int, [_P, _I32, _I32, _P, _P, _DP, _P, _I32]),

@@ -339,7 +339,8 @@ int ensure_batch(sg_handle* h) {
   const int nt = h->d.nt;
   size_t free_b = 0, total_b = 0;
   SG_CK(cudaMemGetInfo(&free_b, &total_b));
-  double budget = h->d.mem_budget_bytes > 0 ? h->d.mem_budget_bytes : 0.9 * (double)free_b;
+  // default: half of the free memory, leaving room for the caller's tensors
+  double budget = h->d.mem_budget_bytes > 0 ? h->d.mem_budget_bytes : 0.5 * (double)free_b;
   budget -= 4.0 * (h->plane + h->ldx + h->tail) * h->esz + (64 << 20);  // statics + slack
   int K = h->d.checkpoint_every > 0 ? h->d.checkpoint_every
                                     : std::max(1, (int)std::ceil(std::sqrt((double)nt)));
@@ -1159,6 +1160,18 @@ bool born_cached_covers(const sg_handle* h, int b0, int cnt) {
   return h->born_hist && b0 >= h->born_b0 && b0 + cnt <= h->born_b0 + h->born_count;
 }
 
+// Next batch [b0, b0 + cnt) of [b0, end) that lies entirely inside or entirely
+// outside the cached background range.
+int born_next_batch(const sg_handle* h, int b0, int end) {
+  int lim = end;
+  if (h->born_hist) {
+    const int c0 = h->born_b0, c1 = h->born_b0 + h->born_count;
+    if (b0 >= c0 && b0 < c1) lim = std::min(end, c1);
+    else if (b0 < c0) lim = std::min(end, c0);
+  }
+  return std::min(h->B, lim - b0);
+}
+
 template <typename T>
 int born_cache_t(sg_handle* h, int shot0, int count) {
   SG_TRY(ensure_batch(h));
@@ -1167,6 +1180,13 @@ int born_cache_t(sg_handle* h, int shot0, int count) {
   h->born_b0 = -1;
   h->born_count = 0;
   const size_t per = (size_t)h->d.nt * h->hplane * h->esz;
+  // cache as many shots as fit (the rest are recomputed per apply)
+  size_t free_b = 0, total_b = 0;
+  SG_CK(cudaMemGetInfo(&free_b, &total_b));
+  const double room = 0.8 * (double)free_b - (double)(2ull << 30);  // leave room for callers
+  count = (int)std::max(0.0, std::min((double)count, std::floor(room / (double)per)));
+  if (const char* e = getenv("SG_BORN_CACHE_MAX")) count = std::min(count, std::max(0, atoi(e)));
+  if (count == 0) return SG_OK;
   SG_TRY(dalloc(h, &h->born_hist, per * count));
   h->born_b0 = shot0;
   h->born_count = count;
@@ -1197,8 +1217,8 @@ int born_forward_t(sg_handle* h, int shot0, int count, const void* m_r, void* ou
   SG_TRY(set_born_scale<T>(h, m_r));
   const int nt = h->d.nt;
   const size_t gper = (size_t)nt * h->d.n_rec * h->esz;
-  for (int b0 = shot0; b0 < shot0 + count; b0 += h->B) {
-    const int cnt = std::min(h->B, shot0 + count - b0);
+  for (int b0 = shot0, cnt = 0; b0 < shot0 + count; b0 += cnt) {
+    cnt = born_next_batch(h, b0, shot0 + count);
     if (born_cached_covers(h, b0, cnt)) {
       // scattered field driven by the cached a0 history (seisopt/wavesim.py:289-290)
       SG_TRY(zero_fields(h, true, false, cnt));
@@ -1260,8 +1280,8 @@ int born_adjoint_core(sg_handle* h, int shot0, int count, const void* data, int 
   SG_CK(cudaMemsetAsync(h->scal, 0, sizeof(double), h->stream));
   const int nt = h->d.nt;
   const size_t gper = (size_t)nt * h->d.n_rec * h->esz;
-  for (int b0 = shot0; b0 < shot0 + count; b0 += h->B) {
-    const int cnt = std::min(h->B, shot0 + count - b0);
+  for (int b0 = shot0, cnt = 0; b0 < shot0 + count; b0 += cnt) {
+    cnt = born_next_batch(h, b0, shot0 + count);
     if (mode_resid == 1) {
       SG_TRY(born_forward_t<T>(h, b0, cnt, m_r, h->gath));
       // born_forward_t copied gathers onto themselves; form the residual in place
@@ -1762,6 +1782,13 @@ int sg_adjoint_history(sg_handle* h, const void* ybar, void* v) {
   SG_TRY(check_handle(h));
   if (!ybar || !v) return fail(SG_ERR_ARG, "null argument");
   return SG_DISPATCH(h, adjoint_history_t, h, ybar, v);
+}
+
+int sg_born_cached(sg_handle* h, int32_t* shot0, int32_t* count) {
+  if (!h) return fail(SG_ERR_ARG, "null handle");
+  if (shot0) *shot0 = h->born_hist ? h->born_b0 : 0;
+  if (count) *count = h->born_hist ? h->born_count : 0;
+  return SG_OK;
 }
 
 int sg_query(sg_handle* h, int32_t* batch, int32_t* recon, double* bytes) {

@@ -147,18 +147,13 @@ class BornKernel:
         self.born_applies = 0
         self.adjoint_applies = 0
         s0, cnt = self._range()
+        self.cached = 0  # shots with a cached background history
         if cache is True or cache == "auto":
-            try:
-                self.ws.born_cache((s0, cnt))
-                self.cached = True
-            except MemoryError:
-                raise
-            except Exception:
-                if cache is True:
-                    raise
-                self.cached = False
-        else:
-            self.cached = False
+            # caches as many shots as fit in HBM; the rest are recomputed
+            self.ws.born_cache((s0, cnt))
+            self.cached = self.ws.born_cached()[1]
+            if cache is True and self.cached < cnt:
+                raise MemoryError(f"only {self.cached} of {cnt} background histories fit")
 
     def _range(self):
         if self.shard is None:

@@ -270,6 +270,12 @@ class Propagator:
         self._stream()
         _lib.check(self.lib.sg_born_cache(self.h, s0, cnt, 1 if enable else 0), "born_cache")
 
+    def born_cached(self):
+        """(first shot, number of shots) whose background history is in HBM."""
+        s0, cnt = C.c_int32(), C.c_int32()
+        _lib.check(self.lib.sg_born_cached(self.h, C.byref(s0), C.byref(cnt)), "born_cached")
+        return s0.value, cnt.value
+
     def born_forward(self, m_r, shots=None):
         torch = _torch()
         s0, cnt = self._range(shots)

@@ -439,3 +439,29 @@ def test_shot_ranges_sum_to_full_gradient():
     pb.born_cache()
     assert rel(pb.born_forward(m_r).cpu().numpy(), d_ref.cpu().numpy()) <= 1e-13
     assert rel(pb.born_adjoint(d_ref).cpu().numpy(), pn.born_adjoint(d_ref).cpu().numpy()) <= 1e-12
+
+
+def test_partial_born_cache(monkeypatch):
+    """Only part of the background histories cached (memory-limited): Born
+    forward, adjoint and LSRTM gradient equal the uncached results."""
+    _, wavesim = _api()
+    case = c1(8)
+    g = case["gold"]
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    rng = np.random.default_rng(9)
+    m_r = rng.standard_normal(grid.shape) * 1e-9
+    ref = wavesim.Propagator(grid, geom, wav, cfg, dtype="float64", batch=2)
+    ref.set_model(g["m_init"])
+    d = ref.born_forward(m_r)
+    img = ref.born_adjoint(d)
+    lv, lg = ref.lsrtm_gradient(m_r * 0.3, d)
+    monkeypatch.setenv("SG_BORN_CACHE_MAX", "3")
+    p = wavesim.Propagator(grid, geom, wav, cfg, dtype="float64", batch=2)
+    p.set_model(g["m_init"])
+    p.born_cache()
+    assert p.born_cached() == (0, 3)
+    assert rel(p.born_forward(m_r).cpu().numpy(), d.cpu().numpy()) <= 1e-13
+    assert rel(p.born_adjoint(d).cpu().numpy(), img.cpu().numpy()) <= 1e-12
+    lv2, lg2 = p.lsrtm_gradient(m_r * 0.3, d)
+    assert abs(lv2 - lv) <= 1e-12 * abs(lv)
+    assert rel(lg2.cpu().numpy(), lg.cpu().numpy()) <= 1e-12
