@@ -50,6 +50,9 @@ constexpr int kHalo = 4;
 #ifndef SG_STCS
 #define SG_STCS 0
 #endif
+#ifndef SG_STAGES
+#define SG_STAGES 2
+#endif
 #ifndef SG_FP32_MINB
 #define SG_FP32_MINB 3
 #endif
@@ -95,6 +98,8 @@ struct StepArgs {
   const T* inj_w;
   const T* ybar;          // adjoint data at this step (+ b*ybar_stride + r)
   int64_t ybar_stride;
+  const T* inj_dense;     // R^T y of this step on the receiver row band
+  int64_t inj_dense_stride;  // (+ b*stride + rr*nxp + j); nullptr: CSR walk
   T* image;               // per-group image planes (stride image_stride)
   int64_t image_stride;
   T* vhist;               // optional v history (adjoint_solve keep_v)
@@ -258,7 +263,7 @@ struct Smem {
   static constexpr int HALO = ((SW * SH + A - 1) / A) * A;
   static constexpr int TILE = kBX * kTH;           // multiple of 128 B
   static constexpr int STAGE = HALO + (ADJ ? 2 : 1) * TILE;
-  static constexpr int BYTES = 2 * STAGE * (int)sizeof(T);
+  static constexpr int BYTES = SG_STAGES * STAGE * (int)sizeof(T);
 };
 
 template <typename T, int R, bool ADJ>
@@ -287,7 +292,8 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
   constexpr bool VHIST = ADJ && (FL & FL_VHIST) != 0;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sbase = reinterpret_cast<T*>(smem_raw);
-  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t bar[SG_STAGES];
+  constexpr int NS = SG_STAGES;
 
   const int tid = threadIdx.y * kBX + threadIdx.x;
   const int grp = blockIdx.y;
@@ -323,13 +329,13 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
   constexpr bool LOAD_HIST = ADJ && HIST;
 
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+#pragma unroll
+    for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
     fence_barrier_init();
   }
   __syncthreads();
   auto issue = [&](int k) {
-    const int s = k & 1;
+    const int s = k % NS;
     T* st = sbase + s * SM::STAGE;
     const int b = b0 + k;
     constexpr uint32_t bytes =
@@ -389,11 +395,12 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
   // everything below reads or writes fields/states of the previous step
   pdl_wait();
   pdl_launch_dependents();
-  if (tid == 0) issue(0);
+  if (tid == 0)
+    for (int k = 0; k < NS - 1 && k < nb; ++k) issue(k);
 
   for (int k = 0; k < nb; ++k) {
     const int b = b0 + k;
-    if (tid == 0 && k + 1 < nb) issue(k + 1);
+    if (tid == 0 && k + NS - 1 < nb) issue(k + NS - 1);
 
     // does this tile hold a source tap of shot b?  (CTA-uniform)
     bool src_here = false;
@@ -415,8 +422,8 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
     const T* __restrict__ gin = nullptr;
     if (GSRC) gin = a.gsrc + (int64_t)b * a.gsrc_stride + o0;
 
-    mbar_wait(&bar[k & 1], (k >> 1) & 1);
-    const T* st = sbase + (k & 1) * SM::STAGE;
+    mbar_wait(&bar[k % NS], (k / NS) & 1);
+    const T* st = sbase + (k % NS) * SM::STAGE;
     // this thread's column, from tile row rb - R
     const T* sc = st + (rb + HO) * SW + threadIdx.x + kHalo;
     const T* sst = st + SM::HALO + rb * kBX + threadIdx.x;
@@ -479,9 +486,13 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
               if (rr >= 0 && rr < a.inj_nrows) {
                 // R^T y: duplicate taps accumulate (np.add.at, seisopt/wavesim.py:229)
                 const int cell = rr * a.nxp + j;
-                const int p1 = a.inj_ptr[cell + 1];
-                for (int p = a.inj_ptr[cell]; p < p1; ++p)
-                  lp += a.inj_w[p] * a.ybar[(int64_t)b * a.ybar_stride + a.inj_rec[p]];
+                if (a.inj_dense != nullptr) {
+                  lp += a.inj_dense[(int64_t)b * a.inj_dense_stride + cell];
+                } else {
+                  const int p1 = a.inj_ptr[cell + 1];
+                  for (int p = a.inj_ptr[cell]; p < p1; ++p)
+                    lp += a.inj_w[p] * a.ybar[(int64_t)b * a.ybar_stride + a.inj_rec[p]];
+                }
               }
             }
             const T so = dd[qq] * sv + lp;
@@ -493,7 +504,7 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
         }
       }
     }
-    __syncthreads();  // stage (k & 1) is free for shot k + 2
+    __syncthreads();  // stage (k % NS) is free for shot k + NS
   }
   if (LOAD_HIST) {
 #pragma unroll

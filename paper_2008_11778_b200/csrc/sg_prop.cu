@@ -141,6 +141,25 @@ __global__ void k_residual(const T* __restrict__ f, const T* __restrict__ g, T* 
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// R^T y for every step on the receiver row band:
+//   dense[b][n][rr][j] = sum_{p in CSR(rr, j)} w_p ybar[b][n][rec_p]
+// in np.add.at order (seisopt/wavesim.py:228-229).  Turns the adjoint step's
+// dependent CSR walk into one coalesced load per band cell.
+template <typename T>
+__global__ void k_inj_dense(const T* __restrict__ ybar, T* __restrict__ dense, int64_t rows,
+                            int nrec, int ncell, const int* __restrict__ ptr,
+                            const int* __restrict__ rec, const T* __restrict__ w) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncell) return;
+  const int p0 = ptr[c], p1 = ptr[c + 1];
+  for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+    T acc = T(0);
+    const T* y = ybar + row * nrec;
+    for (int p = p0; p < p1; ++p) acc += w[p] * y[rec[p]];
+    dense[row * ncell + c] = acc;
+  }
+}
+
 // out[0] += scale * sum(part[0..n))  -- fixed order, one block
 __global__ void k_finish_sum(const double* __restrict__ part, int n, double scale,
                              double* out) {
@@ -262,6 +281,7 @@ struct sg_handle {
   int* tile_rec = nullptr;
   int* rec_rc = nullptr;
   void* gath = nullptr;
+  void* inj_dense = nullptr;  // (B, nt, inj_nrows, nxp) when the band is narrow
   void* hist = nullptr;
   void* ckpt = nullptr;
   void* img = nullptr;
@@ -319,16 +339,21 @@ void free_batch(sg_handle* h) {
   drop_graphs(h);
   h->tmaps.clear();
   void** bufs[] = {(void**)&h->bsrc_rc, &h->bsrc_w, &h->u0, &h->u1, &h->inc, &h->inc2, &h->l0,
-                   &h->l1, &h->w, &h->w2, &h->gath, &h->hist, &h->ckpt, &h->img, &h->acc_img,
+                   &h->l1, &h->w, &h->w2, &h->gath, &h->inj_dense, &h->hist, &h->ckpt, &h->img, &h->acc_img,
                    (void**)&h->part, (void**)&h->scal};
   for (auto p : bufs) dfree(p);
   h->B = 0;
 }
 
+// receivers on at most this many padded rows get a dense per-step injection array
+constexpr int kDenseInjRows = 16;
+bool dense_injection(const sg_handle* h) { return h->inj_nrows <= kDenseInjRows; }
+
 // bytes per shot for the batch buffers in a given reconstruction mode
 double per_shot_bytes(const sg_handle* h, int recon, int K, int ncp) {
   const double e = h->esz;
   double b = 8.0 * h->plane + (double)h->d.nt * h->d.n_rec + 2.0 * h->hplane;
+  if (dense_injection(h)) b += (double)h->d.nt * h->inj_nrows * h->nxp;
   if (recon == SG_RECON_FULL) b += (double)h->d.nt * h->hplane;
   else b += (double)K * h->hplane + 2.0 * ncp * h->plane;
   return b * e + 64.0;
@@ -376,6 +401,8 @@ int ensure_batch(sg_handle* h) {
   SG_TRY(dalloc(h, &h->w, fb));
   SG_TRY(dalloc(h, &h->w2, fb));
   SG_TRY(dalloc(h, &h->gath, (size_t)B * nt * h->d.n_rec * e));
+  if (dense_injection(h))
+    SG_TRY(dalloc(h, &h->inj_dense, (size_t)B * nt * h->inj_nrows * h->nxp * e));
   SG_TRY(dalloc(h, &h->hist, (size_t)B * h->hist_steps * h->hplane * e));
   if (recon == SG_RECON_CHECKPOINT)
     SG_TRY(dalloc(h, &h->ckpt, (size_t)ncp * 2 * span_bytes(h, B)));
@@ -833,6 +860,11 @@ int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, con
   int n = n_hi - 1;
   while (n >= n_lo) {
     const T* yb = p.inject ? reinterpret_cast<const T*>(h->gath) + (int64_t)n * h->d.n_rec : nullptr;
+    if (p.inject && h->inj_dense) {
+      a.inj_dense = reinterpret_cast<const T*>(h->inj_dense) +
+                    (int64_t)n * h->inj_nrows * h->nxp;
+      a.inj_dense_stride = (int64_t)h->d.nt * h->inj_nrows * h->nxp;
+    }
     if (use2 && n - 1 >= n_lo) {
       a2.cur = cur;
       a2.n0 = n;
@@ -959,6 +991,21 @@ int residual(sg_handle* h, int cnt, const T* obs, int mode) {
   const double scale = (mode == 1) ? 0.5 : 0.5 * h->d.dt;
   k_finish_sum<<<1, 1024, 0, h->stream>>>(h->part, blocks, scale, h->scal);
   count_launch(2);
+  SG_CK(cudaGetLastError());
+  return SG_OK;
+}
+
+// expand the adjoint data now in h->gath into the dense band array
+template <typename T>
+int fill_injection(sg_handle* h, int cnt) {
+  if (!h->inj_dense) return SG_OK;
+  const int ncell = h->inj_nrows * h->nxp;
+  const int64_t rows = (int64_t)cnt * h->d.nt;
+  dim3 grid(cdiv(ncell, 128), (unsigned)std::min<int64_t>(rows, 8192));
+  k_inj_dense<T><<<grid, 128, 0, h->stream>>>(
+      reinterpret_cast<const T*>(h->gath), reinterpret_cast<T*>(h->inj_dense), rows,
+      h->d.n_rec, ncell, h->inj_ptr, h->inj_rec, reinterpret_cast<const T*>(h->inj_w));
+  count_launch();
   SG_CK(cudaGetLastError());
   return SG_OK;
 }
@@ -1128,6 +1175,7 @@ int fwi_gradient_t(sg_handle* h, int shot0, int count, const void* obs, double* 
     SG_TRY(do_forward_batch<T>(h, b0, cnt, true));
     SG_TRY(residual<T>(h, cnt, reinterpret_cast<const T*>((const char*)obs + (b0 - shot0) * per),
                        0));
+    SG_TRY(fill_injection<T>(h, cnt));
     SG_TRY(do_adjoint_batch<T>(h, cnt, nullptr, 0));
     SG_TRY(reduce_images<T>(h, cnt));
   }
@@ -1286,8 +1334,10 @@ int born_adjoint_core(sg_handle* h, int shot0, int count, const void* data, int 
       SG_TRY(born_forward_t<T>(h, b0, cnt, m_r, h->gath));
       // born_forward_t copied gathers onto themselves; form the residual in place
       SG_TRY(residual<T>(h, cnt, reinterpret_cast<const T*>((const char*)d_r + (b0 - shot0) * gper), 1));
+      SG_TRY(fill_injection<T>(h, cnt));
     } else {
       SG_TRY(copy_gathers_in<T>(h, (const char*)data + (size_t)(b0 - shot0) * gper, cnt));
+      SG_TRY(fill_injection<T>(h, cnt));
     }
     if (born_cached_covers(h, b0, cnt)) {
       const void* base = (char*)h->born_hist + (size_t)(b0 - h->born_b0) * nt * h->hplane * h->esz;
@@ -1365,6 +1415,7 @@ int adjoint_history_t(sg_handle* h, const void* ybar, void* vout) {
   void* tmp = nullptr;
   SG_TRY(dalloc(h, &tmp, (size_t)nt * h->hplane * h->esz));
   SG_TRY(copy_gathers_in<T>(h, ybar, 1));
+  SG_TRY(fill_injection<T>(h, 1));
   SG_TRY(zero_fields(h, false, true, 1));
   AdjPlan p;
   p.vhist = tmp;
