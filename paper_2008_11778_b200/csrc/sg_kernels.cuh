@@ -328,6 +328,14 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
   const int j0 = txi * kBX;
   constexpr bool LOAD_HIST = ADJ && HIST;
 
+  // source taps of the group's shots, staged once (static data, PDL-safe)
+  __shared__ int s_src[8 * 8];
+  __shared__ T s_sw[8 * 4];
+  if (!ADJ && a.src_rc != nullptr) {
+    if (tid < nb * 8) s_src[tid] = a.src_rc[b0 * 8 + tid];
+    if (tid < nb * 4) s_sw[tid] = a.src_w[b0 * 4 + tid];
+  }
+
   if (tid == 0) {
 #pragma unroll
     for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
@@ -407,7 +415,7 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
     if (!ADJ && a.src_rc != nullptr) {
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        const int r = a.src_rc[(b * 4 + t) * 2], c = a.src_rc[(b * 4 + t) * 2 + 1];
+        const int r = s_src[(k * 4 + t) * 2], c = s_src[(k * 4 + t) * 2 + 1];
         src_here |= (r >= i0 && r < i0 + kTH && c >= j0 && c < j0 + kBX);
       }
     }
@@ -468,8 +476,8 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
               const int i = ib + qq;
 #pragma unroll
               for (int t = 0; t < 4; ++t) {
-                const int r = a.src_rc[(b * 4 + t) * 2], c = a.src_rc[(b * 4 + t) * 2 + 1];
-                if (r == i && c == j) acc += a.amp * a.src_w[b * 4 + t] * im[qq];
+                const int r = s_src[(k * 4 + t) * 2], c = s_src[(k * 4 + t) * 2 + 1];
+                if (r == i && c == j) acc += a.amp * s_sw[k * 4 + t] * im[qq];
               }
             }
   #if SG_STCS

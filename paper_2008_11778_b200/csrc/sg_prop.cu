@@ -424,11 +424,11 @@ int ensure_batch(sg_handle* h) {
 // busiest CTA processes ceil(items / slots) * G shots.  Minimise that
 // critical path times the amortisation overhead.
 int group_for(const sg_handle* h, int count) {
-  if (h->d.group > 0) return std::max(1, std::min(h->d.group, count));
+  if (h->d.group > 0) return std::max(1, std::min({h->d.group, count, 8}));
   static int env = -1;
   if (env < 0) {
     const char* e = getenv("SG_GROUP");
-    env = e ? std::max(0, atoi(e)) : 0;
+    env = e ? std::max(0, std::min(8, atoi(e))) : 0;
   }
   if (env > 0) return std::max(1, std::min(env, count));
   const int slots = h->nsm * (h->esz == 4 ? 3 : 2);
@@ -685,7 +685,7 @@ int step2_args(sg_handle* h, Step2Args<T>& a, void* F0, void* F1, void* S0, void
 
 // shots per group for the two-step kernel (2 CTAs/SM)
 int group2_for(const sg_handle* h, int count) {
-  if (h->d.group > 0) return std::max(1, std::min(h->d.group, count));
+  if (h->d.group > 0) return std::max(1, std::min({h->d.group, count, 8}));
   const int slots = h->nsm * 2;
   int best = 1;
   double best_cost = 1e300;
