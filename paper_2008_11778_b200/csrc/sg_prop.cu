@@ -1170,15 +1170,34 @@ int fwi_gradient_t(sg_handle* h, int shot0, int count, const void* obs, double* 
   SG_CK(cudaMemsetAsync(h->scal, 0, sizeof(double), h->stream));
   SG_CK(cudaMemsetAsync(h->acc_img, 0, (size_t)h->hplane * h->esz, h->stream));
   const size_t per = (size_t)h->d.nt * h->d.n_rec * h->esz;
+  // optional phase timing (env SG_PHASE_TIMING=1): forward / glue / adjoint
+  static const bool timing = getenv("SG_PHASE_TIMING") != nullptr;
+  cudaEvent_t ev[5] = {};
+  if (timing)
+    for (auto& e : ev) cudaEventCreate(&e);
   for (int b0 = shot0; b0 < shot0 + count; b0 += h->B) {
     const int cnt = std::min(h->B, shot0 + count - b0);
+    if (timing) cudaEventRecord(ev[0], h->stream);
     SG_TRY(do_forward_batch<T>(h, b0, cnt, true));
+    if (timing) cudaEventRecord(ev[1], h->stream);
     SG_TRY(residual<T>(h, cnt, reinterpret_cast<const T*>((const char*)obs + (b0 - shot0) * per),
                        0));
     SG_TRY(fill_injection<T>(h, cnt));
+    if (timing) cudaEventRecord(ev[2], h->stream);
     SG_TRY(do_adjoint_batch<T>(h, cnt, nullptr, 0));
+    if (timing) cudaEventRecord(ev[3], h->stream);
     SG_TRY(reduce_images<T>(h, cnt));
+    if (timing) {
+      cudaEventRecord(ev[4], h->stream);
+      cudaEventSynchronize(ev[4]);
+      float t[4];
+      for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+      fprintf(stderr, "[sg] batch %d+%d: forward %.3f ms, residual+injection %.3f ms, "
+              "adjoint %.3f ms, image reduce %.3f ms\n", b0, cnt, t[0], t[1], t[2], t[3]);
+    }
   }
+  if (timing)
+    for (auto& e : ev) cudaEventDestroy(e);
   SG_TRY(fold_out<T>(h, grad, accumulate));
   if (misfit) {
     SG_CK(cudaMemcpyAsync(misfit, h->scal, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -1466,9 +1485,15 @@ int time_kernel_t(sg_handle* h, int which, int count, int reps, float* ms) {
       }
       for (int r = 0; r < reps; ++r) SG_TRY(enq_forward<T>(h, s, count, n + (r & 1), n + (r & 1) + 1, p));
     } else {
+      // walk the history like a sweep does (a different, L2-cold plane per
+      // launch) so the timing includes the streaming history read
       AdjPlan p;
-      p.hist = main_hist(h, n);
-      for (int r = 0; r < reps; ++r) SG_TRY(enq_adjoint<T>(h, s, count, n + 1, n, p));
+      p.hist = main_hist(h, 0);
+      p.hist.rotate = true;
+      for (int r = 0; r < reps; ++r) {
+        const int m = (int)((h->d.nt - 1 - r % h->d.nt) % std::max<int64_t>(1, h->hist_steps));
+        SG_TRY(enq_adjoint<T>(h, s, count, m + 1, m, p));
+      }
     }
     return SG_OK;
   };
