@@ -7,8 +7,10 @@ Workload (default, BASELINE.json configs[2] = "C3"): one complete FWI gradient
 per step -- 30 shots, 201x601 grid (241x641 padded), nt 4000, 8th-order
 stencil, fp32, 20-cell sponge: forward sweep with history store, residual +
 misfit, adjoint sweep with fused imaging, image reduction, fold, and (N > 1)
-one all-reduce.  Shots are sharded over the N ranks (total work fixed ->
-"strong" scaling).  Synthetic seeded layered-fault model (the paper's Marmousi
+one all-reduce.  Shots are sharded over the N ranks in contiguous blocks.
+C3/C4 scale weakly (each rank owns the config's shot count; the survey has
+30*N / 60*N evenly spaced shots); C5 is the fixed 240-shot survey split over
+the ranks (strong); --scaling overrides.  Synthetic seeded layered-fault model (the paper's Marmousi
 is not available offline).
 
 metric: Gcell-updates/s = 2 * shots * nt * padded cells per gradient (forward +
@@ -115,15 +117,32 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
-def build_case(config):
+def build_case(config, n_shots=None):
     from paper_2008_11778_b200 import synthetic
     if config == "c1":
         case = synthetic.c1_case(order=8)
         case["dtype"] = "float64"
         return case
-    case = synthetic.layered_case(config)
+    case = synthetic.layered_case(config, n_shots=n_shots)
     case["dtype"] = "float32"
     return case
+
+
+BASE_SHOTS = {"c1": 5, "c3": 30, "c4": 60, "c5": 240}
+
+
+def scaling_mode(args):
+    """C3/C4: weak (each rank owns the config's full shot set, the survey grows
+    with N).  C5 is quoted as a fixed 240-shot survey sharded over 1..8 GPUs
+    (strong); C1 is a parity case (strong, replicas of 5 shots)."""
+    if args.scaling != "auto":
+        return args.scaling
+    return "weak" if args.config in ("c3", "c4") else "strong"
+
+
+def total_shots(args, world):
+    base = BASE_SHOTS[args.config]
+    return base * world if scaling_mode(args) == "weak" else base
 
 
 def padded_cells(case):
@@ -174,7 +193,8 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * statistics.median(times), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": scaling_mode(args), "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {"workload": workload_name(args.config), "sample": sample},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": sample},
@@ -242,7 +262,7 @@ def run_lsrtm(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    case = build_case("c4")
+    case = build_case("c4", total_shots(args, world))
     geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
     S, nt = geom.n_sources, geom.nt
     shard = shards.ShotShard.from_env(S) if world > 1 else None
@@ -289,7 +309,8 @@ def run_lsrtm(args):
             "metric": "LSRTM wave-stencil Gcell-updates/s (Born fwd + adjoint)",
             "value": cells * args.steps / (ms / 1e3) / 1e9, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": scaling_mode(args), "vs_baseline": None,
+            "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": "C4 LSRTM gradient: layered-fault 201x601 @15 m, 60 shots, "
                                    "601 rec, nt 6000, 15 Hz, 8th order, fp32",
@@ -317,7 +338,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    case = build_case(args.config)
+    case = build_case(args.config, total_shots(args, world))
     geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
     S, nt = geom.n_sources, geom.nt
     shard = shards.ShotShard.from_env(S) if world > 1 else None
@@ -427,9 +448,10 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": scaling_mode(args), "vs_baseline": None,
             "dtype": "f32" if es == 4 else "f64", "data": "synthetic",
-            "config": {"workload": workload_name(args.config), "shots": S, "nt": nt,
+            "config": {"workload": workload_name(args.config), "shots": S,
+                       "shots_per_rank": local_shots, "nt": nt,
                        "padded_cells": C, "order": cfg.order, "recon": q["recon"],
                        "shots_per_launch": q["batch"],
                        "l2": l2},
@@ -569,6 +591,9 @@ def main():
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"],
+                    help="weak: config shot count per rank (C3/C4 default); "
+                         "strong: config shot count sharded over ranks (C1/C5 default)")
     args = ap.parse_args()
     if args.config == "c2":
         return run_c2(args) if args.impl != "reference" else run_reference_c2(args)
