@@ -673,20 +673,71 @@ def minimize_aa(problem, p0, memory, eta=None, budget=None, max_iters=None,
     return dict(p=p, rows=rows, eta=eta, lambdas=lams, inequality_log=ineq, iterates=iterates)
 
 
-def minimize_sd(problem, p0, eta=None, max_iters=None):
-    """Fixed-step steepest descent -- anderson.py:235-280 (line_search=False)."""
+def armijo_search(value_fn, p, direction, grad_p, value_p, initial_step, c1, max_bt,
+                  budget_ok=None):
+    """Armijo backtracking -- seisopt/optim/linesearch.py:29-70.
+    Returns (step, success)."""
+    slope = float(np.dot(direction, grad_p))
+    if slope >= 0.0 or initial_step <= 0.0:
+        raise ValueError("not a descent direction / non-positive step")
+    s = float(initial_step)
+    for _ in range(max_bt):
+        if budget_ok is not None and not budget_ok():
+            return 0.0, False
+        f = value_fn(p + s * direction)
+        if np.isfinite(f) and f <= value_p + c1 * s * slope:
+            return s, True
+        s *= 0.5
+    return 0.0, False
+
+
+def minimize_sd(problem, p0, eta=None, max_iters=None, line_search=False, c1=1e-4,
+                max_backtracks=10, budget=None):
+    """Steepest descent -- anderson.py:235-280 (fixed step, or Armijo
+    backtracking from eta with the eta * 0.5**max_backtracks fallback)."""
     p = np.asarray(p0, dtype=np.float64).copy()
     rows, k = [], 0
     while True:
+        if not _budget_ok(problem, budget, 1.0):
+            break
         val, g = problem.value_and_grad(p)
         if eta is None:
             eta = default_eta(p, g)
         gn = float(np.linalg.norm(g))
         done = max_iters is not None and k >= max_iters
-        rows.append((k, val, gn, problem.counters.grad_evals, problem.counters.obj_evals,
-                     0.0 if done else eta))
+        step = 0.0
+        if not done:
+            step = eta
+            if line_search:
+                s, ok = armijo_search(problem.value, p, -g, g, val, eta, c1, max_backtracks,
+                                      lambda: _budget_ok(problem, budget, 0.5))
+                step = s if ok else eta * 0.5 ** max_backtracks
+        rows.append((k, val, gn, problem.counters.grad_evals, problem.counters.obj_evals, step))
         if done:
             break
-        p = p - eta * g
+        p = p - step * g
         k += 1
     return dict(p=p, rows=rows, eta=eta)
+
+
+def aa_run(operator, p0, memory, iterations, beta=1.0, residual_tol=0.0):
+    """Generic AA of a fixed-point operator -- anderson.py:168-203.
+    Returns (iterates, residual_norms, combined_norms)."""
+    p = np.asarray(p0, dtype=np.float64)
+    win = AAWindowOracle(p.size, memory)
+    its, res, comb = [p.copy()], [], []
+    for _ in range(iterations):
+        win.push(p, operator(p))
+        fk = float(np.linalg.norm(win.f_k))
+        if win.m_k == 0:
+            pn, cn = aa_step(win, beta), fk
+        else:
+            w = aa_weights(win)
+            pn, cn = aa_step(win, beta, w), w[2]
+        its.append(pn)
+        res.append(fk)
+        comb.append(cn)
+        p = pn
+        if residual_tol and fk <= residual_tol:
+            break
+    return its, res, comb

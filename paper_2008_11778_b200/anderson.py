@@ -371,9 +371,11 @@ def _blend_search(problem, value_k, grad_k, p_k, p_bar, p_tilde, c1, max_backtra
     return 0.0, p_bar
 
 
-def minimize_sd(problem, p0, eta=None, budget=None, max_iters=None, grad_tol=0.0):
-    """Fixed-step steepest descent (seisopt/optim/anderson.py:235-280,
-    line_search=False) on device vectors."""
+def minimize_sd(problem, p0, eta=None, budget=None, max_iters=None, grad_tol=0.0,
+                line_search=False, c1=1e-4, max_backtracks=10):
+    """Steepest descent with a fixed step (default) or Armijo backtracking
+    (seisopt/optim/anderson.py:235-280) on device vectors."""
+    from .quasi_newton import backtracking_line_search
     torch = _torch()
     numpy_out = not isinstance(p0, torch.Tensor)
     prop = getattr(problem, "prop", None)
@@ -387,17 +389,107 @@ def minimize_sd(problem, p0, eta=None, budget=None, max_iters=None, grad_tol=0.0
         if not _budget_allows(problem, budget, 1.0):
             break
         value, grad = problem.value_and_grad(p)
+        grad = grad if isinstance(grad, torch.Tensor) else torch.as_tensor(grad, device=p.device)
         grad = grad.to(p.dtype).reshape(-1).contiguous()
         if eta is None:
             eta = default_eta(p, grad)
         grad_norm = vec_stats(grad)["norm"]
         done = (grad_tol and grad_norm <= grad_tol) or (max_iters is not None and k >= max_iters)
+        step = 0.0
+        if not done:
+            if line_search:
+                res = backtracking_line_search(
+                    problem.value, p, -grad, grad, value, initial_step=eta, c1=c1,
+                    max_backtracks=max_backtracks,
+                    budget_ok=lambda: _budget_allows(problem, budget, 0.5))
+                step = res.step if res.success else eta * 0.5 ** max_backtracks
+            else:
+                step = eta
         report.append(iteration=k, objective=value, grad_norm=grad_norm,
                       grad_evals=problem.counters.grad_evals,
-                      obj_evals=problem.counters.obj_evals, step=0.0 if done else eta)
+                      obj_evals=problem.counters.obj_evals, step=step)
         if done:
             break
-        p = vec_axpby(1.0, p, -eta, grad)
+        p = vec_axpby(1.0, p, -step, grad)
         k += 1
     return OptimizeResult(p=p.double().cpu().numpy() if numpy_out else p, report=report,
                           extras={"eta": eta})
+
+
+# ---------------------------------------------------------------------------
+# generic fixed-point acceleration (seisopt/optim/anderson.py:155-220)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class FixedPointTrace:
+    """Iterates and residual diagnostics of a fixed-point run
+    (seisopt/optim/anderson.py:155-165)."""
+
+    iterates: list = field(default_factory=list)
+    residual_norms: list = field(default_factory=list)
+    combined_norms: list = field(default_factory=list)
+
+    @property
+    def final(self):
+        return self.iterates[-1]
+
+
+def aa_run(operator, p0, memory, iterations, beta=1.0, residual_tol=0.0, *, dtype=None,
+           device=None):
+    """Anderson acceleration of a fixed-point operator
+    (seisopt/optim/anderson.py:168-203): per iteration push (p, G(p)), record
+    ||f_k|| and the minimised combined residual, step with beta.
+
+    The window lives on the GPU.  NumPy ``p0`` gives NumPy float64 iterates and
+    the operator is called with NumPy vectors (like the reference); a torch
+    CUDA ``p0`` keeps every iterate on the device and the operator receives
+    torch tensors."""
+    torch = _torch()
+    numpy_io = not isinstance(p0, torch.Tensor)
+    if dtype is None:
+        dtype = torch.float64 if numpy_io else p0.dtype
+    dev = device if device is not None else (
+        torch.device("cuda", torch.cuda.current_device()) if numpy_io else p0.device)
+    p = torch.as_tensor(np.asarray(p0, np.float64) if numpy_io else p0, device=dev,
+                        dtype=dtype).reshape(-1).contiguous().clone()
+    window = AAWindow(p.numel(), memory, dtype=p.dtype, device=p.device)
+
+    def host(x):
+        return x.double().cpu().numpy() if numpy_io else x
+
+    trace = FixedPointTrace(iterates=[host(p.clone())])
+    for _ in range(iterations):
+        g_value = operator(host(p))
+        g_dev = torch.as_tensor(g_value, device=p.device).to(p.dtype).reshape(-1).contiguous()
+        window.push(p, g_dev)
+        fk_norm = window.f_k_norm()
+        if window.m_k == 0:
+            p_next = aa_step(window, beta=beta)
+            combined = fk_norm
+        else:
+            weights = aa_weights(window)
+            p_next = aa_step(window, beta=beta, weights=weights)
+            combined = weights.residual_norm
+        trace.iterates.append(host(p_next))
+        trace.residual_norms.append(fk_norm)
+        trace.combined_norms.append(combined)
+        p = p_next
+        if residual_tol and fk_norm <= residual_tol:
+            break
+    return trace
+
+
+def multisecant_oracle(p_mat, d_mat):
+    """Minimiser S of ||S + I||_F subject to S D = P (closed form
+    S = -I + (P + D)(D^T D)^{-1} D^T; seisopt/optim/anderson.py:206-222).  A
+    dense n x n host helper for tests of the AA update, as in the reference."""
+    p_mat = np.atleast_2d(np.asarray(p_mat, dtype=np.float64))
+    d_mat = np.atleast_2d(np.asarray(d_mat, dtype=np.float64))
+    if p_mat.shape != d_mat.shape:
+        raise ValueError("P and D must have matching shapes")
+    n, m = d_mat.shape
+    if np.linalg.matrix_rank(d_mat) < m:
+        raise np.linalg.LinAlgError("D is rank deficient; multi-secant oracle unavailable")
+    coeff = np.linalg.solve(d_mat.T @ d_mat, d_mat.T)
+    return -np.eye(n) + (p_mat + d_mat) @ coeff

@@ -219,8 +219,52 @@ def make_aa_window():
         step_half=np.stack([r["step_half"] for r in recs]), **versions())
 
 
+def make_aa_run():
+    """aa_run on a contractive affine fixed point G(p) = M p + c (beta 1 and
+    0.7), and Armijo steepest descent on the small FWI problem."""
+    use_order(2)
+    rng = np.random.default_rng(5)
+    n = 120
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    mat = q @ np.diag(np.linspace(-0.9, 0.95, n)) @ q.T
+    c = rng.standard_normal(n)
+    p0 = rng.standard_normal(n)
+    out = dict(n=n, mat=mat, c=c, p0=p0)
+    for tag, memory, beta, iters in (("b1", 5, 1.0, 14), ("b07", 3, 0.7, 12), ("m0", 0, 1.0, 6)):
+        tr = A.aa_run(lambda p: mat @ p + c, p0, memory, iters, beta=beta)
+        out[f"{tag}_iterates"] = np.stack(tr.iterates)
+        out[f"{tag}_res"] = np.array(tr.residual_norms)
+        out[f"{tag}_comb"] = np.array(tr.combined_norms)
+    tr = A.aa_run(lambda p: mat @ p + c, p0, 4, 40, residual_tol=0.05)
+    out["tol_iterates"] = np.stack(tr.iterates)
+    np.savez_compressed(os.path.join(HERE, "aa_run.npz"), **out, **versions())
+    # steepest descent with the Armijo search (minimize_sd(line_search=True))
+    use_order(8)
+    grid, model, geom, wav, cfg = small_setup(8, True)
+    c_true = model.velocity.copy()
+    c_true[18:24, 25:35] *= 1.06
+    obs = G.fwi_synthetic(VelocityModel.from_velocity(grid, c_true), wav, geom, cfg)
+    res = A.minimize_sd(G.FwiObjective(grid, obs, wav, geom, cfg), model.m.ravel(),
+                        eta=None, max_iters=3, line_search=True)
+    rows = np.array([[r.iteration, r.objective, r.grad_norm, r.grad_evals, r.obj_evals,
+                      r.step] for r in res.report.rows])
+    big = A.minimize_sd(G.FwiObjective(grid, obs, wav, geom, cfg), model.m.ravel(),
+                        eta=6.0 * res.extras["eta"], max_iters=2, line_search=True,
+                        max_backtracks=2)
+    big_rows = np.array([[r.iteration, r.objective, r.grad_norm, r.grad_evals, r.obj_evals,
+                          r.step] for r in big.report.rows])
+    np.savez_compressed(os.path.join(HERE, "sd_linesearch.npz"), rows=rows, final=res.p,
+                        eta=res.extras["eta"], big_rows=big_rows, big_final=big.p,
+                        **versions())
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
     make_aa_window()
+    make_aa_run()
     for order in (2, 8):
         for top in (True, False):
             make_small(order, top)

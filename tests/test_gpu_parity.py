@@ -254,6 +254,52 @@ def test_minimize_aa_trajectory_fp64():
     assert rel(r0.p, gold["sd_final"]) <= F64
 
 
+def test_aa_run_matches_reference():
+    """aa_run (seisopt/optim/anderson.py:168-203) with the GPU window, NumPy
+    and device-tensor operators, against the reference's own run."""
+    from paper_2008_11778_b200 import anderson
+    g = golden("aa_run")
+    mat, c = g["mat"], g["c"]
+    mat_d = torch.as_tensor(mat, device="cuda")
+    c_d = torch.as_tensor(c, device="cuda")
+    for tag, memory, beta, iters in (("b1", 5, 1.0, 14), ("b07", 3, 0.7, 12), ("m0", 0, 1.0, 6)):
+        tr = anderson.aa_run(lambda p: mat @ p + c, g["p0"], memory, iters, beta=beta)
+        assert isinstance(tr.final, np.ndarray)
+        assert rel(np.stack(tr.iterates), g[f"{tag}_iterates"]) <= F64
+        assert np.allclose(tr.residual_norms, g[f"{tag}_res"], rtol=1e-10)
+        assert np.allclose(tr.combined_norms, g[f"{tag}_comb"], rtol=1e-8)
+        trd = anderson.aa_run(lambda p: mat_d @ p + c_d, torch.as_tensor(g["p0"], device="cuda"),
+                              memory, iters, beta=beta)
+        assert trd.final.is_cuda
+        assert rel(torch.stack(trd.iterates).cpu().numpy(), g[f"{tag}_iterates"]) <= F64
+    tr = anderson.aa_run(lambda p: mat @ p + c, g["p0"], 4, 40, residual_tol=0.05)
+    assert len(tr.iterates) == len(g["tol_iterates"])
+
+
+def test_sd_armijo_trajectory_fp64():
+    """minimize_sd(line_search=True) on the GPU objective vs the reference run."""
+    gradients, _ = _api()
+    from paper_2008_11778_b200 import anderson
+    gold = golden("sd_linesearch")
+    case = small_case(8, True)
+    g = case["gold"]
+
+    def obj():
+        return gradients.FwiObjective(case["grid"], list(g["obs"]), case["wavelet"],
+                                      case["geometry"], case["config"])
+
+    for kw, rows_k, final_k in (({}, "rows", "final"),
+                                (dict(eta=6.0 * float(gold["eta"]), max_iters=2,
+                                      max_backtracks=2), "big_rows", "big_final")):
+        kw.setdefault("max_iters", 3)
+        res = anderson.minimize_sd(obj(), g["m"].ravel(), line_search=True, **kw)
+        rows = np.array([[r.iteration, r.objective, r.grad_norm, r.grad_evals, r.obj_evals,
+                          r.step] for r in res.report.rows])
+        assert np.array_equal(rows[:, [0, 3, 4]], gold[rows_k][:, [0, 3, 4]])
+        assert np.allclose(rows[:, [1, 2, 5]], gold[rows_k][:, [1, 2, 5]], rtol=1e-9)
+        assert rel(res.p, gold[final_k]) <= F64
+
+
 @pytest.mark.parametrize("group", [1, 2, 3])
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_shot_groups_agree(group, dtype):

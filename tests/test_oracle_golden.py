@@ -104,3 +104,49 @@ def test_aa_fwi_trajectory():
     obj0 = oracle.FwiOracleObjective(make, list(gs["obs"]), wav.samples, geom.nt, grid.shape)
     r0 = oracle.minimize_aa(obj0, gs["m"].ravel(), memory=0, max_iters=3)
     assert rel(r0["p"], g["sd_final"]) == 0.0
+
+
+def test_aa_run_fixed_point():
+    """Generic fixed-point AA (anderson.py:168-203) against the reference run."""
+    g = golden("aa_run")
+    mat, c = g["mat"], g["c"]
+
+    def op(p):
+        return mat @ p + c
+
+    for tag, memory, beta, iters in (("b1", 5, 1.0, 14), ("b07", 3, 0.7, 12), ("m0", 0, 1.0, 6)):
+        its, res, comb = oracle.aa_run(op, g["p0"], memory, iters, beta=beta)
+        assert rel(np.stack(its), g[f"{tag}_iterates"]) <= 1e-13
+        assert np.allclose(res, g[f"{tag}_res"], rtol=1e-13)
+        assert np.allclose(comb, g[f"{tag}_comb"], rtol=1e-12)
+        # the combined residual never exceeds the plain one
+        assert all(cn <= fk * (1 + 1e-12) for cn, fk in zip(comb, res))
+    its, _, _ = oracle.aa_run(op, g["p0"], 4, 40, residual_tol=0.05)
+    assert len(its) == len(g["tol_iterates"])
+    assert rel(np.stack(its), g["tol_iterates"]) <= 1e-13
+
+
+def test_sd_armijo_trajectory():
+    """minimize_sd(line_search=True) (anderson.py:235-280 + linesearch.py:29-70)."""
+    g = golden("sd_linesearch")
+    case = small_case(8, True)
+    gs = case["gold"]
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+
+    def make(m):
+        return oracle_setup(m, grid, geom, cfg)
+
+    obs = oracle.fwi_synthetic(make(gs["m_true"]), wav.samples, geom.nt)
+    obj = oracle.FwiOracleObjective(make, obs, wav.samples, geom.nt, grid.shape)
+    res = oracle.minimize_sd(obj, gs["m"].ravel(), max_iters=3, line_search=True)
+    rows = np.array(res["rows"])
+    assert np.array_equal(rows[:, [0, 3, 4]], g["rows"][:, [0, 3, 4]])
+    assert np.allclose(rows[:, [1, 2, 5]], g["rows"][:, [1, 2, 5]], rtol=1e-12)
+    assert rel(res["p"], g["final"]) <= 1e-12
+    obj = oracle.FwiOracleObjective(make, obs, wav.samples, geom.nt, grid.shape)
+    big = oracle.minimize_sd(obj, gs["m"].ravel(), eta=6.0 * float(g["eta"]), max_iters=2,
+                             line_search=True, max_backtracks=2)
+    rows = np.array(big["rows"])
+    assert np.array_equal(rows[:, [0, 3, 4]], g["big_rows"][:, [0, 3, 4]])
+    assert np.allclose(rows[:, [1, 2, 5]], g["big_rows"][:, [1, 2, 5]], rtol=1e-12)
+    assert rel(big["p"], g["big_final"]) <= 1e-12
