@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libseisgpu.so")
 SG_OK, SG_ERR_ARG, SG_ERR_STABILITY, SG_ERR_EMPTY = 0, 1, 2, 3
 SG_ERR_CUDA, SG_ERR_OOM, SG_ERR_MODEL, SG_ERR_STATE = 4, 5, 6, 7
 SG_F32, SG_F64 = 4, 8
-SG_RECON_FULL, SG_RECON_CHECKPOINT, SG_RECON_AUTO = 0, 1, 2
+SG_RECON_FULL, SG_RECON_CHECKPOINT, SG_RECON_AUTO, SG_RECON_BOUNDARY = 0, 1, 2, 3
 
 
 class EmptyWindowError(Exception):

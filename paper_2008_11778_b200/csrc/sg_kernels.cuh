@@ -32,29 +32,32 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace sg {
 
 constexpr int kGuard = 4;         // zero guard rows above/below each plane
 constexpr int kTileRowsMax = 64;  // tail padding covers tiles up to this height
-constexpr int kBX = 64, kBY = 4, kNY = 8, kTH = kBY * kNY;  // 64 x 32 tile, 256 threads
+// 64 x 32 tile, 256 threads = 32 column pairs x 8 row groups of kNY rows
+constexpr int kBX = 64, kTX = 32, kTY = 8, kNY = 4, kTH = kTY * kNY;
+constexpr int kThreads = kTX * kTY;
 // TMA halo boxes are always kHalo wide (the 8th-order radius); the 2nd-order
 // stencil reads the inner ring only.  72 x 40 boxes keep every TMA row a
 // multiple of 16 B for fp32 and fp64.
 constexpr int kHalo = 4;
-#ifndef SG_HINT_FIELD
-#define SG_HINT_FIELD 0
+// TMA pipeline depth (shot stages in shared memory) of the fp32 one-step
+// kernels; fp64 and the fused reverse kernel use 2
+#ifndef SG_FWD_STAGES
+#define SG_FWD_STAGES 3
 #endif
-#ifndef SG_HINT_HIST
-#define SG_HINT_HIST 0
-#endif
-#ifndef SG_STCS
-#define SG_STCS 0
-#endif
-#ifndef SG_STAGES
-#define SG_STAGES 2
+#ifndef SG_ADJ_STAGES
+#define SG_ADJ_STAGES 3
 #endif
 #ifndef SG_FP32_MINB
 #define SG_FP32_MINB 3
+#endif
+#ifndef SG_ADJ_MINB
+#define SG_ADJ_MINB 2
 #endif
 
 template <typename T>
@@ -104,7 +107,39 @@ struct StepArgs {
   int64_t image_stride;
   T* vhist;               // optional v history (adjoint_solve keep_v)
   int64_t vhist_stride;
+  // ---- boundary-saving reconstruction (FL_BAND) -------------------------------
+  // The forward stores u_n on the sponge frame ("band": rows < bT or >= nzp-bB,
+  // cols < bL or >= nxp-bR; every cell with damp < 1 lies inside it) at each
+  // step; the adjoint runs the forward backwards in the undamped interior,
+  //   a_n = inv_m L u_n (+ source),  inc_n = inc_{n+1} - dt^2 a_n,
+  //   u_{n-1} = u_n - inc_n,
+  // takes frame cells from the store and images against the recomputed a_n.
+  CUtensorMap r_halo[2];  // ADJ: forward field buffers, halo box
+  CUtensorMap r_stile;    // ADJ: forward increment state, tile box
+  T* rf[2];               // forward field buffers (row 0, col 0, shot 0)
+  T* rstate;              // forward increment: inc_{n+1} in, inc_n out (in place)
+  int rcur;               // ADJ: read rf[rcur] (u_n), write rf[rcur ^ 1] (u_{n-1})
+  T* band;                // band store, shot stride band_stride, nb cells per step
+  int64_t band_stride;
+  int band_slot;          // FWD: slot of u_n; ADJ: slot of u_{n-1} (< 0: none)
+  int bT, bB, bL, bR, nb;
 };
+
+// frame geometry of the band store (a subset of StepArgs' fields)
+struct BandGeo {
+  int nzp, nxp, ldx, bT, bB, bL, bR, nb;
+};
+
+// index of padded cell (i, j) in a band-store step, or -1 outside the frame
+template <typename G>
+__device__ __forceinline__ int band_index(const G& a, int i, int j) {
+  if (i < a.bT) return i * a.nxp + j;
+  if (i >= a.nzp - a.bB) return (a.bT + i - (a.nzp - a.bB)) * a.nxp + j;
+  const int base = (a.bT + a.bB) * a.nxp + (i - a.bT) * (a.bL + a.bR);
+  if (j < a.bL) return base + j;
+  if (j >= a.nxp - a.bR) return base + a.bL + j - (a.nxp - a.bR);
+  return -1;
+}
 
 // ---- PTX helpers -----------------------------------------------------------
 
@@ -235,6 +270,16 @@ struct V2<float> {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
     return r;
   }
+  __device__ __forceinline__ float lo() const {
+    float a, b;
+    split(a, b);
+    return a;
+  }
+  __device__ __forceinline__ float hi() const {
+    float a, b;
+    split(a, b);
+    return b;
+  }
 };
 
 template <>
@@ -251,24 +296,62 @@ struct V2<double> {
   __device__ __forceinline__ static V2 fma(V2 a, V2 b, V2 c) {
     return V2{__fma_rn(a.x, b.x, c.x), __fma_rn(a.y, b.y, c.y)};
   }
+  __device__ __forceinline__ double lo() const { return x; }
+  __device__ __forceinline__ double hi() const { return y; }
 };
+
+// aligned pair loads / stores (shared or global; 8 B for fp32, 16 B for fp64)
+template <typename T>
+struct Vec2;
+template <>
+struct Vec2<float> {
+  using type = float2;
+};
+template <>
+struct Vec2<double> {
+  using type = double2;
+};
+template <typename T>
+__device__ __forceinline__ V2<T> lds2(const T* p) {
+  const auto v = *reinterpret_cast<const typename Vec2<T>::type*>(p);
+  return V2<T>::make(v.x, v.y);
+}
+template <typename T>
+__device__ __forceinline__ V2<T> ldg2(const T* p) {
+  const auto v = __ldg(reinterpret_cast<const typename Vec2<T>::type*>(p));
+  return V2<T>::make(v.x, v.y);
+}
+template <typename T>
+__device__ __forceinline__ void st2(T* p, V2<T> v) {
+  typename Vec2<T>::type o;
+  v.split(o.x, o.y);
+  *reinterpret_cast<typename Vec2<T>::type*>(p) = o;
+}
 
 // shared-memory plan of one CTA (element counts; every region 128-B aligned):
 // two stages of {halo'd field tile, state tile[, history tile (adjoint)]}
-template <typename T, int R, bool ADJ>
+// (RB: the fused reverse-forward + adjoint step of boundary-saving
+// reconstruction; a stage then holds {adjoint halo, w tile, u halo, inc tile})
+template <typename T, bool ADJ, bool RB>
+__host__ __device__ constexpr int step_stages() {
+  return (sizeof(T) != 4 || RB) ? 2 : (ADJ ? SG_ADJ_STAGES : SG_FWD_STAGES);
+}
+
+template <typename T, int R, bool ADJ, bool RB = false>
 struct Smem {
   static constexpr int SW = kBX + 2 * kHalo;
   static constexpr int SH = kTH + 2 * kHalo;
   static constexpr int A = 128 / (int)sizeof(T);  // elements per 128 B
   static constexpr int HALO = ((SW * SH + A - 1) / A) * A;
   static constexpr int TILE = kBX * kTH;           // multiple of 128 B
-  static constexpr int STAGE = HALO + (ADJ ? 2 : 1) * TILE;
-  static constexpr int BYTES = SG_STAGES * STAGE * (int)sizeof(T);
+  static constexpr int STAGE = RB ? 2 * HALO + 2 * TILE : HALO + (ADJ ? 2 : 1) * TILE;
+  static constexpr int NS = step_stages<T, ADJ, RB>();
+  static constexpr int BYTES = NS * STAGE * (int)sizeof(T);
 };
 
-template <typename T, int R, bool ADJ>
+template <typename T, int R, bool ADJ, bool RB = false>
 __host__ __device__ constexpr int step_smem_bytes() {
-  return Smem<T, R, ADJ>::BYTES;
+  return Smem<T, R, ADJ, RB>::BYTES;
 }
 
 // ----------------------------------------------------------------------------
@@ -279,23 +362,46 @@ constexpr int FL_HIST = 1;    // FWD: store a_n; ADJ: image against a_n
 constexpr int FL_GSRC = 2;    // FWD: Born grid source a0_n * gscale
 constexpr int FL_VHIST = 4;   // ADJ: store v_n (adjoint_solve keep_v)
 constexpr int FL_GATHER = 8;  // FWD: receiver sampling blocks present
+constexpr int FL_BAND = 16;   // FWD: store u_n on the sponge frame; ADJ: reverse-
+                              // reconstruct the forward and image against it
+
+// CTAs per SM the step kernel is built for (fp32 RB stages need 77 KB smem)
+template <typename T, bool ADJ, int FL>
+__host__ __device__ constexpr int step_min_blocks() {
+  // (fp64 RB stages are 154 KB: one CTA per SM)
+  return sizeof(T) != 4 ? ((ADJ && (FL & FL_BAND)) ? 1 : 2)
+                        : ((ADJ && (FL & FL_BAND)) ? 2 : (ADJ ? SG_ADJ_MINB : SG_FP32_MINB));
+}
+
+// R^T y of one cell by a walk over its CSR taps (receiver bands too wide for
+// the dense per-step array); out of line to keep the step's registers free
+template <typename T>
+__device__ __noinline__ T inj_csr(const StepArgs<T>& a, int b, int cell, T lv) {
+  const int p1 = a.inj_ptr[cell + 1];
+  for (int p = a.inj_ptr[cell]; p < p1; ++p)
+    lv += a.inj_w[p] * a.ybar[(int64_t)b * a.ybar_stride + a.inj_rec[p]];
+  return lv;
+}
 
 template <typename T, int R, bool ADJ, int FL>
-__global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
+__global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
     k_step(const __grid_constant__ StepArgs<T> a) {
-  using SM = Smem<T, R, ADJ>;
+  constexpr bool RB = ADJ && (FL & FL_BAND) != 0;     // fused reverse + adjoint
+  constexpr bool BSAVE = !ADJ && (FL & FL_BAND) != 0;  // forward band store
+  using SM = Smem<T, R, ADJ, RB>;
+  using P = V2<T>;
   constexpr int SW = SM::SW;
-  constexpr int NCOL = kNY + 2 * R;
-  constexpr int HO = kHalo - R;  // offset of the radius-R window inside the halo box
+  constexpr int NCOL = kNY + 2 * R;  // rows of the vertical window
+  constexpr int HO = kHalo - R;      // offset of the radius-R window inside the halo box
   constexpr bool HIST = (FL & FL_HIST) != 0;
   constexpr bool GSRC = !ADJ && (FL & FL_GSRC) != 0;
   constexpr bool VHIST = ADJ && (FL & FL_VHIST) != 0;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sbase = reinterpret_cast<T*>(smem_raw);
-  __shared__ __align__(8) uint64_t bar[SG_STAGES];
-  constexpr int NS = SG_STAGES;
+  constexpr int NS = SM::NS;
+  __shared__ __align__(8) uint64_t bar[NS];
 
-  const int tid = threadIdx.y * kBX + threadIdx.x;
+  const int tid = threadIdx.y * kTX + threadIdx.x;
   const int grp = blockIdx.y;
   const int b0 = grp * a.G;
   const int nb = min(a.G, a.count - b0);
@@ -308,8 +414,8 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
       // (seisopt/wavesim.py:225-226, sampled before the update, :287)
       const T* __restrict__ u = a.f[a.cur];
       const int total = nb * a.nrec;
-      for (int e = ((int)blockIdx.x - a.ntiles) * (kBX * kBY) + tid; e < total;
-           e += a.rec_blocks * (kBX * kBY)) {
+      for (int e = ((int)blockIdx.x - a.ntiles) * kThreads + tid; e < total;
+           e += a.rec_blocks * kThreads) {
         const int bb = b0 + e / a.nrec;
         const int r = e - (e / a.nrec) * a.nrec;
         const T* ub = u + (int64_t)bb * a.plane;
@@ -326,12 +432,14 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
   const int txi = blockIdx.x - tzi * a.tiles_x;
   const int i0 = tzi * kTH;
   const int j0 = txi * kBX;
-  constexpr bool LOAD_HIST = ADJ && HIST;
+  constexpr bool LOAD_HIST = ADJ && HIST && !RB;
+  constexpr bool IMG = LOAD_HIST || RB;  // adjoint image accumulation
+  constexpr bool SRC = !ADJ || RB;       // forward acceleration with point source
 
   // source taps of the group's shots, staged once (static data, PDL-safe)
   __shared__ int s_src[8 * 8];
   __shared__ T s_sw[8 * 4];
-  if (!ADJ && a.src_rc != nullptr) {
+  if (SRC && a.src_rc != nullptr) {
     if (tid < nb * 8) s_src[tid] = a.src_rc[b0 * 8 + tid];
     if (tid < nb * 4) s_sw[tid] = a.src_w[b0 * 4 + tid];
   }
@@ -347,59 +455,62 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
     T* st = sbase + s * SM::STAGE;
     const int b = b0 + k;
     constexpr uint32_t bytes =
-        (SM::SW * SM::SH + (LOAD_HIST ? 2 : 1) * SM::TILE) * (uint32_t)sizeof(T);
+        RB ? (2 * SM::SW * SM::SH + 2 * SM::TILE) * (uint32_t)sizeof(T)
+           : (SM::SW * SM::SH + (LOAD_HIST ? 2 : 1) * SM::TILE) * (uint32_t)sizeof(T);
     mbar_expect_tx(&bar[s], bytes);
     // rows of a guarded plane: data row i lives at plane row kGuard + i
-    // the working set (fields, state) is kept in L2; the history stream,
-    // read once, is evicted first so it does not push the working set out
-#if SG_HINT_FIELD
-    tma_load_3d_hint(st, &a.f_halo[a.cur], &bar[s], j0 - kHalo, kGuard + i0 - kHalo, b,
-                     kEvictLast);
-    tma_load_3d_hint(st + SM::HALO, &a.s_tile, &bar[s], j0, kGuard + i0, b, kEvictLast);
-#else
     tma_load_3d(st, &a.f_halo[a.cur], &bar[s], j0 - kHalo, kGuard + i0 - kHalo, b);
     tma_load_3d(st + SM::HALO, &a.s_tile, &bar[s], j0, kGuard + i0, b);
-#endif
-    if (LOAD_HIST) {
-#if SG_HINT_HIST
-      tma_load_3d_hint(st + SM::HALO + SM::TILE, &a.h_tile, &bar[s], j0, i0,
-                       b * a.hist_steps + a.hist_slot, kEvictFirst);
-#else
+    if (LOAD_HIST)
       tma_load_3d(st + SM::HALO + SM::TILE, &a.h_tile, &bar[s], j0, i0,
                   b * a.hist_steps + a.hist_slot);
-#endif
+    if (RB) {
+      tma_load_3d(st + SM::HALO + SM::TILE, &a.r_halo[a.rcur], &bar[s], j0 - kHalo,
+                  kGuard + i0 - kHalo, b);
+      tma_load_3d(st + 2 * SM::HALO + SM::TILE, &a.r_stile, &bar[s], j0, kGuard + i0, b);
     }
   };
-  const int j = j0 + threadIdx.x;
-  const bool vj = j < a.nxp;
+  // this thread: columns (j, j + 1), rows ib .. ib + kNY - 1; every update is
+  // done on the column pair with packed f32x2 arithmetic
+  const int j = j0 + 2 * threadIdx.x;
+  const bool vj0 = j < a.nxp;
+  const bool vj1 = j + 1 < a.nxp;
   const int rb = threadIdx.y * kNY;  // first tile row owned by this thread
   const int ib = i0 + rb;
-  const int nq = vj ? max(0, min(kNY, a.nzp - ib)) : 0;
+  const int nq = vj0 ? max(0, min(kNY, a.nzp - ib)) : 0;
   const int o0 = ib * a.ldx + j;     // offset of this thread's first cell
   const int ldx = a.ldx;
+  // frame test is CTA-uniform per tile (band kernels only)
+  const bool tile_band = (BSAVE || RB) && (i0 < a.bT || i0 + kTH > a.nzp - a.bB ||
+                                           j0 < a.bL || j0 + kBX > a.nxp - a.bR);
 
   // per-cell model data, reused for every shot of the group; the image
   // accumulator starts from the stored image (prefetched, lands during shot 0)
-  T im[kNY], dd[kNY], img[kNY];
-  const T pxj = vj ? a.px[j] : T(0);
+  P im[kNY], dd[kNY];
+  T img[2 * kNY];
+  const T pxj0 = a.px[j], pxj1 = a.px[j + 1];  // zero beyond nxp (profile tail)
   // Prologue (may overlap the previous step under PDL): model data and the
   // image accumulator of this launch's parity, last written two launches ago
   // (complete: the previous grid signalled its dependents only after its own
   // griddepcontrol.wait).
   T* ig = nullptr;
-  if (LOAD_HIST) ig = a.image + (int64_t)grp * a.image_stride + o0;
+  if (IMG) ig = a.image + (int64_t)grp * a.image_stride + o0;
 #pragma unroll
   for (int q = 0; q < kNY; ++q) {
     if (q < nq) {
-      im[q] = a.inv_m[o0 + q * ldx];
-      dd[q] = a.pz[ib + q] * pxj;
-      img[q] = LOAD_HIST ? ig[q * ldx] : T(0);
+      im[q] = ldg2(a.inv_m + o0 + q * ldx);
+      const T pz = a.pz[ib + q];
+      dd[q] = P::make(pz * pxj0, pz * pxj1);
+      img[2 * q] = IMG ? ig[q * ldx] : T(0);
+      img[2 * q + 1] = (IMG && vj1) ? ig[q * ldx + 1] : T(0);
     } else {
-      im[q] = T(0);
-      dd[q] = T(0);
-      img[q] = T(0);
+      im[q] = P::make(T(0), T(0));
+      dd[q] = P::make(T(0), T(0));
+      img[2 * q] = T(0);
+      img[2 * q + 1] = T(0);
     }
   }
+  const P dt2p = P::make(a.dt2, a.dt2);
   // everything below reads or writes fields/states of the previous step
   pdl_wait();
   pdl_launch_dependents();
@@ -412,7 +523,7 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
 
     // does this tile hold a source tap of shot b?  (CTA-uniform)
     bool src_here = false;
-    if (!ADJ && a.src_rc != nullptr) {
+    if (SRC && a.src_rc != nullptr) {
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const int r = s_src[(k * 4 + t) * 2], c = s_src[(k * 4 + t) * 2 + 1];
@@ -429,96 +540,202 @@ __global__ void __launch_bounds__(kBX* kBY, sizeof(T) == 4 ? SG_FP32_MINB : 2)
     if (!ADJ && HIST) hout = a.hist + ((int64_t)b * a.hist_steps + a.hist_slot) * a.hplane + o0;
     const T* __restrict__ gin = nullptr;
     if (GSRC) gin = a.gsrc + (int64_t)b * a.gsrc_stride + o0;
+    T* __restrict__ rout = nullptr;   // RB: u_{n-1}
+    T* __restrict__ rsout = nullptr;  // RB: inc_n
+    const T* __restrict__ bsrc = nullptr;
+    T* __restrict__ bdst = nullptr;
+    if (RB) {
+      rout = a.rf[a.rcur ^ 1] + sb + o0;
+      rsout = a.rstate + sb + o0;
+      if (a.band_slot >= 0) bsrc = a.band + (int64_t)b * a.band_stride + (int64_t)a.band_slot * a.nb;
+    }
+    if (BSAVE) bdst = a.band + (int64_t)b * a.band_stride + (int64_t)a.band_slot * a.nb;
 
     mbar_wait(&bar[k % NS], (k / NS) & 1);
     const T* st = sbase + (k % NS) * SM::STAGE;
-    // this thread's column, from tile row rb - R
-    const T* sc = st + (rb + HO) * SW + threadIdx.x + kHalo;
-    const T* sst = st + SM::HALO + rb * kBX + threadIdx.x;
+    // this thread's column pair in the halo box, from tile row rb - R
+    const T* sc = st + (rb + HO) * SW + kHalo + 2 * threadIdx.x;
+    const T* sst = st + SM::HALO + rb * kBX + 2 * threadIdx.x;
+    const T* scu = st + SM::HALO + SM::TILE + (rb + HO) * SW + kHalo + 2 * threadIdx.x;
+    const T* sinc = st + 2 * SM::HALO + SM::TILE + rb * kBX + 2 * threadIdx.x;
 
     if (nq > 0) {
-      using P = V2<T>;
-      constexpr int NH = kNY / 2;  // cells q and q + NH form one pair
-      T col[NCOL];
-#pragma unroll
-      for (int r = 0; r < NCOL; ++r) col[r] = sc[r * SW];
-#pragma unroll
-      for (int q = 0; q < NH; ++q) {
-        // Laplacian of cells (q, q + NH) in difference form, two per instruction
-        const P uc = P::make(col[q + R], col[q + NH + R]);
-        const T* ra = sc + (q + R) * SW;
-        const T* rbw = sc + (q + NH + R) * SW;
+      // Laplacian of the cell pair of window row q in difference form
+      // sum_k c_k ((u_{-k} - u) + (u_{+k} - u)); vertical neighbours from the
+      // register window, horizontal ones from 8-byte aligned shared loads
+      // (odd offsets re-paired from their aligned neighbours)
+      auto lap2 = [&](const P* w, const T* s, int q) -> P {
+        const P uc = w[q + R];
+        const T* row = s + (q + R) * SW;
+        P xm[R + 1], xp[R + 1];
+        const P m2 = lds2(row - 2), p2 = lds2(row + 2);
+        xm[1] = P::make(m2.hi(), uc.lo());
+        xp[1] = P::make(uc.hi(), p2.lo());
+        if constexpr (R >= 2) {
+          xm[2] = m2;
+          xp[2] = p2;
+        }
+        if constexpr (R >= 4) {
+          const P m4 = lds2(row - 4), p4 = lds2(row + 4);
+          xm[3] = P::make(m4.hi(), m2.lo());
+          xp[3] = P::make(p2.hi(), p4.lo());
+          xm[4] = m4;
+          xp[4] = p4;
+        }
         P lz = P::make(T(0), T(0)), lx = P::make(T(0), T(0));
 #pragma unroll
         for (int kk = 1; kk <= R; ++kk) {
           const P cz = P::make(a.cz[kk], a.cz[kk]);
           const P cx = P::make(a.cx[kk], a.cx[kk]);
-          const P zm = P::make(col[q + R - kk], col[q + NH + R - kk]);
-          const P zp = P::make(col[q + R + kk], col[q + NH + R + kk]);
-          const P xm = P::make(ra[-kk], rbw[-kk]);
-          const P xp = P::make(ra[kk], rbw[kk]);
-          lz = P::fma(cz, (zm - uc) + (zp - uc), lz);
-          lx = P::fma(cx, (xm - uc) + (xp - uc), lx);
+          lz = P::fma(cz, (w[q + R - kk] - uc) + (w[q + R + kk] - uc), lz);
+          lx = P::fma(cx, (xm[kk] - uc) + (xp[kk] - uc), lx);
         }
-        T lap[2], ucs[2];
-        (lz + lx).split(lap[0], lap[1]);
-        uc.split(ucs[0], ucs[1]);
+        return lz + lx;
+      };
+      // forward acceleration a_n of the pair from its Laplacian (+ point source)
+      auto accel = [&](P lp, int q) -> P {
+        P acc = lp * im[q];
+        if (src_here) {
+          const int i = ib + q;
+          T a0, a1, m0, m1;
+          acc.split(a0, a1);
+          im[q].split(m0, m1);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int qq = q + h * NH;
-          if (qq >= nq) continue;
-          const T sv = sst[qq * kBX];
-          T lp = lap[h];
-          if (!ADJ) {
-            if (GSRC) lp += gin[qq * ldx] * a.gscale[o0 + qq * ldx];
-            T acc = lp * im[qq];
-            if (src_here) {
-              const int i = ib + qq;
+          for (int t = 0; t < 4; ++t) {
+            const int r = s_src[(k * 4 + t) * 2], c = s_src[(k * 4 + t) * 2 + 1];
+            if (r == i && c == j) a0 += a.amp * s_sw[k * 4 + t] * m0;
+            if (r == i && c == j + 1) a1 += a.amp * s_sw[k * 4 + t] * m1;
+          }
+          acc = P::make(a0, a1);
+        }
+        return acc;
+      };
+      // frame cells of row q: band-store offsets (or -1) of columns j, j + 1
+      auto band2 = [&](int q, int& bi0, int& bi1) {
+        bi0 = band_index(a, ib + q, j);
+        bi1 = vj1 ? band_index(a, ib + q, j + 1) : -1;
+      };
+
+      P col[NCOL];
 #pragma unroll
-              for (int t = 0; t < 4; ++t) {
-                const int r = s_src[(k * 4 + t) * 2], c = s_src[(k * 4 + t) * 2 + 1];
-                if (r == i && c == j) acc += a.amp * s_sw[k * 4 + t] * im[qq];
-              }
-            }
-  #if SG_STCS
-          if (HIST) __stcs(hout + qq * ldx, acc);  // streaming store: evict first
-#else
-          if (HIST) hout[qq * ldx] = acc;
-#endif
-            const T so = dd[qq] * (sv + a.dt2 * acc);
-            sout[qq * ldx] = so;
-            fout[qq * ldx] = dd[qq] * ucs[h] + so;
-          } else {
-            if (inj_here) {
-              const int rr = ib + qq - a.inj_row0;
-              if (rr >= 0 && rr < a.inj_nrows) {
-                // R^T y: duplicate taps accumulate (np.add.at, seisopt/wavesim.py:229)
-                const int cell = rr * a.nxp + j;
+      for (int r = 0; r < NCOL; ++r) col[r] = lds2(sc + r * SW);
+      P colu[RB ? NCOL : 1];
+      if constexpr (RB) {
+#pragma unroll
+        for (int r = 0; r < NCOL; ++r) colu[r] = lds2(scu + r * SW);
+      }
+      // FULL: all kNY rows and both columns valid (interior tiles) -- no
+      // per-row tests, unmasked pair stores
+      auto rows = [&](auto full_tag) {
+        constexpr bool FULL = decltype(full_tag)::value;
+#pragma unroll
+      for (int q = 0; q < kNY; ++q) {
+        if (!FULL && q >= nq) continue;
+        auto put = [&](T* p, P v) {  // store a pair (only the valid half at the edge)
+          if (FULL || vj1) st2(p, v);
+          else p[0] = v.lo();
+        };
+        const P ucs = col[q + R];
+        const P sv = lds2(sst + q * kBX);
+        P lp = lap2(col, sc, q);
+        if (!ADJ) {
+          if (GSRC) lp = P::fma(ldg2(gin + q * ldx), ldg2(a.gscale + o0 + q * ldx), lp);
+          const P acc = accel(lp, q);
+          if (BSAVE && tile_band) {
+            int bi0, bi1;
+            band2(q, bi0, bi1);
+            if (bi0 >= 0) bdst[bi0] = ucs.lo();
+            if (bi1 >= 0) bdst[bi1] = ucs.hi();
+          }
+          if (HIST) put(hout + q * ldx, acc);
+          const P so = P::fma(dt2p, acc, sv) * dd[q];
+          put(sout + q * ldx, so);
+          put(fout + q * ldx, P::fma(dd[q], ucs, so));
+        } else {
+          if (inj_here) {
+            const int rr = ib + q - a.inj_row0;
+            if (rr >= 0 && rr < a.inj_nrows) {
+              // R^T y: duplicate taps accumulate (np.add.at, seisopt/wavesim.py:229)
+              T l0, l1;
+              lp.split(l0, l1);
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                if (h == 1 && !vj1) continue;
+                const int cell = rr * a.nxp + j + h;
+                T add = T(0);
                 if (a.inj_dense != nullptr) {
-                  lp += a.inj_dense[(int64_t)b * a.inj_dense_stride + cell];
+                  add = a.inj_dense[(int64_t)b * a.inj_dense_stride + cell];
+                  (h ? l1 : l0) += add;
                 } else {
-                  const int p1 = a.inj_ptr[cell + 1];
-                  for (int p = a.inj_ptr[cell]; p < p1; ++p)
-                    lp += a.inj_w[p] * a.ybar[(int64_t)b * a.ybar_stride + a.inj_rec[p]];
+                  T& lv = h ? l1 : l0;
+                  lv = inj_csr(a, b, cell, lv);
                 }
               }
+              lp = P::make(l0, l1);
             }
-            const T so = dd[qq] * sv + lp;
-            sout[qq * ldx] = so;
-            fout[qq * ldx] = dd[qq] * ucs[h] + (a.dt2 * im[qq] * dd[qq]) * so;
-            if (LOAD_HIST) img[qq] -= sst[qq * kBX + SM::TILE] * ucs[h];
-            if (VHIST) a.vhist[(int64_t)b * a.vhist_stride + o0 + qq * ldx] = ucs[h];
           }
+          const P so = P::fma(dd[q], sv, lp);
+          put(sout + q * ldx, so);
+          put(fout + q * ldx, P::fma(dd[q], ucs, ((dt2p * im[q]) * dd[q]) * so));
+          T v0, v1;
+          ucs.split(v0, v1);
+          if (LOAD_HIST) {
+            const P hh = lds2(sst + SM::TILE + q * kBX);
+            img[2 * q] -= hh.lo() * v0;
+            img[2 * q + 1] -= hh.hi() * v1;
+          }
+          if constexpr (RB) {
+            // forward run backwards: a_n (bitwise the forward's for the same
+            // u_n), then inc_n and u_{n-1}; frame cells come from the store
+            const P acc = accel(lap2(colu, scu, q), q);
+            img[2 * q] -= acc.lo() * v0;
+            img[2 * q + 1] -= acc.hi() * v1;
+            const P incn = lds2(sinc + q * kBX) - dt2p * acc;
+            put(rsout + q * ldx, incn);
+            P um1 = colu[q + R] - incn;
+            if (bsrc != nullptr && tile_band) {
+              int bi0, bi1;
+              band2(q, bi0, bi1);
+              T w0, w1;
+              um1.split(w0, w1);
+              if (bi0 >= 0) w0 = bsrc[bi0];
+              if (bi1 >= 0) w1 = bsrc[bi1];
+              um1 = P::make(w0, w1);
+            }
+            put(rout + q * ldx, um1);
+          }
+          if (VHIST) put(a.vhist + (int64_t)b * a.vhist_stride + o0 + q * ldx, ucs);
         }
       }
+      };
+      if (nq == kNY && vj1) rows(std::true_type{});
+      else rows(std::false_type{});
     }
     __syncthreads();  // stage (k % NS) is free for shot k + NS
   }
-  if (LOAD_HIST) {
+  if (IMG) {
 #pragma unroll
     for (int q = 0; q < kNY; ++q)
-      if (q < nq) ig[q * ldx] = img[q];
+      if (q < nq) {
+        ig[q * ldx] = img[2 * q];
+        if (vj1) ig[q * ldx + 1] = img[2 * q + 1];
+      }
   }
+}
+
+// Start of a reverse sweep: u_{nt-1} = u_nt - inc_nt inside the frame, the
+// stored band values on it (slot nt-1).  One thread per padded cell.
+template <typename T>
+__global__ void k_band_init(const T* __restrict__ u, const T* __restrict__ inc,
+                            T* __restrict__ out, const T* __restrict__ band,
+                            int64_t band_stride, int slot, BandGeo geo, int64_t plane) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  const int b = blockIdx.z;
+  if (j >= geo.nxp) return;
+  const int64_t o = (int64_t)b * plane + (int64_t)i * geo.ldx + j;
+  const int bi = band_index(geo, i, j);
+  out[o] = bi >= 0 ? band[(int64_t)b * band_stride + (int64_t)slot * geo.nb + bi] : u[o] - inc[o];
 }
 
 }  // namespace sg

@@ -36,7 +36,7 @@ using namespace sg;
 namespace {
 
 constexpr int BX = kBX, TH = kTH;  // 64 x 32 tiles, 256 threads
-constexpr int RB = kBX * kBY;       // threads per block
+constexpr int RB = kThreads;        // threads per block
 constexpr int kSlack = 256;         // column slack for profile arrays
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
@@ -284,6 +284,8 @@ struct sg_handle {
   void* inj_dense = nullptr;  // (B, nt, inj_nrows, nxp) when the band is narrow
   void* hist = nullptr;
   void* ckpt = nullptr;
+  void* band = nullptr;   // BOUNDARY: (B, nt, nb) u on the sponge frame
+  BandGeo bgeo{};         // frame of the band store (set with the sponge)
   void* img = nullptr;
   void* acc_img = nullptr;
   double* part = nullptr;   // reduction partials
@@ -339,7 +341,7 @@ void free_batch(sg_handle* h) {
   drop_graphs(h);
   h->tmaps.clear();
   void** bufs[] = {(void**)&h->bsrc_rc, &h->bsrc_w, &h->u0, &h->u1, &h->inc, &h->inc2, &h->l0,
-                   &h->l1, &h->w, &h->w2, &h->gath, &h->inj_dense, &h->hist, &h->ckpt, &h->img, &h->acc_img,
+                   &h->l1, &h->w, &h->w2, &h->gath, &h->inj_dense, &h->hist, &h->ckpt, &h->band, &h->img, &h->acc_img,
                    (void**)&h->part, (void**)&h->scal};
   for (auto p : bufs) dfree(p);
   h->B = 0;
@@ -355,6 +357,7 @@ double per_shot_bytes(const sg_handle* h, int recon, int K, int ncp) {
   double b = 8.0 * h->plane + (double)h->d.nt * h->d.n_rec + 2.0 * h->hplane;
   if (dense_injection(h)) b += (double)h->d.nt * h->inj_nrows * h->nxp;
   if (recon == SG_RECON_FULL) b += (double)h->d.nt * h->hplane;
+  else if (recon == SG_RECON_BOUNDARY) b += (double)h->hplane + (double)h->d.nt * h->bgeo.nb;
   else b += (double)K * h->hplane + 2.0 * ncp * h->plane;
   return b * e + 64.0;
 }
@@ -377,7 +380,9 @@ int ensure_batch(sg_handle* h) {
   const double full_b = per_shot_bytes(h, SG_RECON_FULL, K, ncp);
   const double ck_b = per_shot_bytes(h, SG_RECON_CHECKPOINT, K, ncp);
   if (recon == SG_RECON_AUTO) recon = (full_b * want <= budget) ? SG_RECON_FULL : SG_RECON_CHECKPOINT;
-  const double per = recon == SG_RECON_FULL ? full_b : ck_b;
+  const double per = recon == SG_RECON_FULL       ? full_b
+                     : recon == SG_RECON_BOUNDARY ? per_shot_bytes(h, recon, K, ncp)
+                                                  : ck_b;
   int B = (int)std::min<double>(want, std::floor(budget / per));
   if (B < 1)
     return fail(SG_ERR_OOM, "one shot needs " + std::to_string(per / 1e9) +
@@ -387,7 +392,8 @@ int ensure_batch(sg_handle* h) {
   h->recon = recon;
   h->K = K;
   h->ncp = ncp;
-  h->hist_steps = recon == SG_RECON_FULL ? nt : K;
+  // BOUNDARY keeps one history slot (the lock-step Born background hand-off)
+  h->hist_steps = recon == SG_RECON_FULL ? nt : (recon == SG_RECON_BOUNDARY ? 1 : K);
   const size_t e = h->esz;
   const size_t fb = ((size_t)h->ldx + (size_t)B * h->plane + h->tail) * e;
   SG_TRY(dalloc(h, (void**)&h->bsrc_rc, (size_t)B * 8 * sizeof(int)));
@@ -406,6 +412,8 @@ int ensure_batch(sg_handle* h) {
   SG_TRY(dalloc(h, &h->hist, (size_t)B * h->hist_steps * h->hplane * e));
   if (recon == SG_RECON_CHECKPOINT)
     SG_TRY(dalloc(h, &h->ckpt, (size_t)ncp * 2 * span_bytes(h, B)));
+  if (recon == SG_RECON_BOUNDARY)
+    SG_TRY(dalloc(h, &h->band, (size_t)B * nt * h->bgeo.nb * e));
   SG_TRY(dalloc(h, &h->img, (size_t)2 * B * h->hplane * e));  // two launch-parity sets
   SG_TRY(dalloc(h, &h->acc_img, (size_t)h->hplane * e));
   h->npart = 1184;
@@ -423,7 +431,7 @@ int ensure_batch(sg_handle* h) {
 // ~20 B per shot-cell); the persistent grid holds `slots` CTAs, so the
 // busiest CTA processes ceil(items / slots) * G shots.  Minimise that
 // critical path times the amortisation overhead.
-int group_for(const sg_handle* h, int count) {
+int group_for(const sg_handle* h, int count, int per_sm = 0) {
   if (h->d.group > 0) return std::max(1, std::min({h->d.group, count, 8}));
   static int env = -1;
   if (env < 0) {
@@ -431,7 +439,7 @@ int group_for(const sg_handle* h, int count) {
     env = e ? std::max(0, std::min(8, atoi(e))) : 0;
   }
   if (env > 0) return std::max(1, std::min(env, count));
-  const int slots = h->nsm * (h->esz == 4 ? 3 : 2);
+  const int slots = h->nsm * (per_sm > 0 ? per_sm : (h->esz == 4 ? 3 : 2));
   int best = 1;
   double best_cost = 1e300;
   for (int G = 1; G <= std::min(8, count); ++G) {
@@ -446,8 +454,8 @@ int group_for(const sg_handle* h, int count) {
   return best;
 }
 
-int ngroups(const sg_handle* h, int count) {
-  const int G = group_for(h, count);
+int ngroups(const sg_handle* h, int count, int per_sm = 0) {
+  const int G = group_for(h, count, per_sm);
   return (count + G - 1) / G;
 }
 
@@ -541,25 +549,33 @@ int step_args(sg_handle* h, StepArgs<T>& a, void* F0, void* F1, void* S0, void* 
   a.inj_ptr = h->inj_ptr;
   a.inj_rec = h->inj_rec;
   a.inj_w = reinterpret_cast<const T*>(h->inj_w);
+  a.bT = h->bgeo.bT;
+  a.bB = h->bgeo.bB;
+  a.bL = h->bgeo.bL;
+  a.bR = h->bgeo.bR;
+  a.nb = h->bgeo.nb;
+  a.band_slot = -1;
   return SG_OK;
 }
 
 template <typename T, int R, bool ADJ, int FL>
 void launch_step_f(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a0) {
   static bool attr = false;
-  constexpr int smem = step_smem_bytes<T, R, ADJ>();
+  constexpr bool RBK = ADJ && (FL & FL_BAND) != 0;
+  constexpr int smem = step_smem_bytes<T, R, ADJ, RBK>();
+  constexpr int per_sm = step_min_blocks<T, ADJ, FL>();
   if (!attr) {
     cudaFuncSetAttribute(k_step<T, R, ADJ, FL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          smem);
     attr = true;
   }
   StepArgs<T> a = a0;
-  a.G = group_for(h, a.count);
+  a.G = group_for(h, a.count, per_sm);
   a.rec_blocks = (a.G * h->d.n_rec + RB - 1) / RB;
   const int extra = (!ADJ && (FL & FL_GATHER)) ? a.rec_blocks : 0;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(h->ntiles + extra, ngroups(h, a.count));
-  cfg.blockDim = dim3(kBX, kBY);
+  cfg.gridDim = dim3(h->ntiles + extra, ngroups(h, a.count, per_sm));
+  cfg.blockDim = dim3(kTX, kTY);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr_pdl[1];
@@ -576,11 +592,17 @@ void launch_step_f(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a0) {
 template <typename T, int R, bool ADJ>
 void launch_step_r(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a) {
   const int fl = (a.hist_on ? FL_HIST : 0) | (a.gsrc ? FL_GSRC : 0) |
-                 (a.vhist ? FL_VHIST : 0) | (a.gather ? FL_GATHER : 0);
+                 (a.vhist ? FL_VHIST : 0) | (a.gather ? FL_GATHER : 0) | (a.band ? FL_BAND : 0);
   if constexpr (ADJ) {
-    if (fl & FL_VHIST) launch_step_f<T, R, ADJ, FL_VHIST>(h, s, a);
+    if (fl & FL_BAND) launch_step_f<T, R, ADJ, FL_BAND>(h, s, a);
+    else if (fl & FL_VHIST) launch_step_f<T, R, ADJ, FL_VHIST>(h, s, a);
     else if (fl & FL_HIST) launch_step_f<T, R, ADJ, FL_HIST>(h, s, a);
     else launch_step_f<T, R, ADJ, 0>(h, s, a);
+  } else if (fl & FL_BAND) {
+    // band-saving forwards: FWI gradient (gathers) and Born background (one-slot history)
+    if (fl & FL_HIST) launch_step_f<T, R, ADJ, FL_BAND | FL_HIST>(h, s, a);
+    else if (fl & FL_GATHER) launch_step_f<T, R, ADJ, FL_BAND | FL_GATHER>(h, s, a);
+    else launch_step_f<T, R, ADJ, FL_BAND>(h, s, a);
   } else {
   switch (fl & (FL_HIST | FL_GSRC | FL_GATHER)) {
     case 0: launch_step_f<T, R, ADJ, 0>(h, s, a); break;
@@ -631,6 +653,7 @@ struct FwdPlan {
   int64_t gsrc_shot = 0;
   int gsrc_n0 = 0;
   bool ckpt_save = false;   // save (u_n, inc_n) at n % K == 0
+  bool band_save = false;   // BOUNDARY: store u_n on the sponge frame every step
   void* fu0 = nullptr;      // field / state buffers (default u0/u1, inc/inc2)
   void* fu1 = nullptr;
   void* fs0 = nullptr;
@@ -746,7 +769,7 @@ int enq_forward(sg_handle* h, cudaStream_t s, int count, int n0, int n1, const F
                 int* curp = nullptr) {
   void* U0 = p.fu0 ? p.fu0 : h->u0;
   void* U1 = p.fu1 ? p.fu1 : h->u1;
-  const bool use2 = two_step_ok(h) && p.gsrc == nullptr;
+  const bool use2 = two_step_ok(h) && p.gsrc == nullptr && !p.band_save;
   void* S0 = p.fs0 ? p.fs0 : h->inc;
   // the one-step kernel reads and writes its own cells only: state in place
   void* S1 = use2 ? (p.fs1 ? p.fs1 : h->inc2) : S0;
@@ -768,6 +791,10 @@ int enq_forward(sg_handle* h, cudaStream_t s, int count, int n0, int n1, const F
   a.hist = reinterpret_cast<T*>(p.hist.base);
   a.hplane = h->hplane;
   a.gather_stride = (int64_t)h->d.nt * h->d.n_rec;
+  if (p.band_save) {
+    a.band = reinterpret_cast<T*>(h->band);
+    a.band_stride = (int64_t)h->d.nt * h->bgeo.nb;
+  }
   Step2Args<T> a2;
   if (use2) {
     SG_TRY(step2_args<T>(h, a2, U0, U1, S0, S1, p.hist.base, p.hist.shots * p.hist.steps));
@@ -813,6 +840,7 @@ int enq_forward(sg_handle* h, cudaStream_t s, int count, int n0, int n1, const F
       if (p.gsrc)
         a.gsrc = reinterpret_cast<const T*>(p.gsrc) + (int64_t)(n - p.gsrc_n0) * h->hplane;
       a.gather = p.gathers ? reinterpret_cast<T*>(h->gath) + (int64_t)n * h->d.n_rec : nullptr;
+      a.band_slot = n;
       launch_step<T, false>(h, s, a);
       n += 1;
     }
@@ -825,6 +853,8 @@ struct AdjPlan {
   HistRef hist;                // imaging history (base nullptr: no imaging)
   bool inject = true;          // y from h->gath (scaled residual / data)
   void* vhist = nullptr;       // optional v store (nt planes, compact rows)
+  bool band_recon = false;     // BOUNDARY: reverse-reconstruct u (u0/u1, inc) and image
+  int rcur0 = 0;               // u_{n_hi-1} lives in {u0, u1}[rcur0]
 };
 
 // Adjoint steps n = n_hi-1 .. n_lo (descending); fields V in l0/l1, states w/w2;
@@ -834,15 +864,36 @@ int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, con
                 int* curp = nullptr) {
   int cur_local = 0;
   int& cur = curp ? *curp : cur_local;
-  const bool use2 = two_step_ok(h) && p.vhist == nullptr;
+  const bool use2 = two_step_ok(h) && p.vhist == nullptr && !p.band_recon;
   void* W1 = use2 ? h->w2 : h->w;  // one-step kernel: state in place
   StepArgs<T> a;
   SG_TRY(step_args<T>(h, a, h->l0, h->l1, h->w, W1, p.hist.base, p.hist.shots * p.hist.steps));
   a.count = count;
   a.ybar_stride = (int64_t)h->d.nt * h->d.n_rec;
-  a.hist_on = p.hist.base != nullptr;
+  a.hist_on = p.hist.base != nullptr && !p.band_recon;
   a.hist_steps = p.hist.steps;
-  a.image = a.hist_on ? reinterpret_cast<T*>(h->img) : nullptr;
+  const bool img_on = a.hist_on || p.band_recon;
+  a.image = img_on ? reinterpret_cast<T*>(h->img) : nullptr;
+  int rcur = p.rcur0;
+  if (p.band_recon) {
+    constexpr int R8 = 4, R2 = 1;
+    if (h->d.order == 8) {
+      SG_TRY((get_map<T, R8>(h, h->u0, MAP_HALO, h->B, &a.r_halo[0])));
+      SG_TRY((get_map<T, R8>(h, h->u1, MAP_HALO, h->B, &a.r_halo[1])));
+      SG_TRY((get_map<T, R8>(h, h->inc, MAP_TILE, h->B, &a.r_stile)));
+    } else {
+      SG_TRY((get_map<T, R2>(h, h->u0, MAP_HALO, h->B, &a.r_halo[0])));
+      SG_TRY((get_map<T, R2>(h, h->u1, MAP_HALO, h->B, &a.r_halo[1])));
+      SG_TRY((get_map<T, R2>(h, h->inc, MAP_TILE, h->B, &a.r_stile)));
+    }
+    a.rf[0] = field<T>(h->u0, h);
+    a.rf[1] = field<T>(h->u1, h);
+    a.rstate = field<T>(h->inc, h);
+    a.band = reinterpret_cast<T*>(h->band);
+    a.band_stride = (int64_t)h->d.nt * h->bgeo.nb;
+    a.src_rc = h->bsrc_rc;
+    a.src_w = reinterpret_cast<const T*>(h->bsrc_w);
+  }
   a.image_stride = h->hplane;
   a.vhist_stride = (int64_t)h->d.nt * h->hplane;
   Step2Args<T> a2;
@@ -879,7 +930,13 @@ int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, con
       a.cur = cur;
       a.ybar = yb;
       // image accumulator set of this launch's parity (PDL-safe, see k_step)
-      if (a.hist_on) a.image = reinterpret_cast<T*>(h->img) + (int64_t)cur * h->B * h->hplane;
+      if (img_on) a.image = reinterpret_cast<T*>(h->img) + (int64_t)cur * h->B * h->hplane;
+      if (p.band_recon) {
+        a.rcur = rcur;
+        a.amp = (T)h->wavelet[n];
+        a.band_slot = n - 1;  // u_{n-1} on the frame (none below step 0)
+        rcur ^= 1;
+      }
       if (a.hist_on) a.hist_slot = p.hist.slot(n);
       a.vhist = p.vhist ? reinterpret_cast<T*>(p.vhist) + (int64_t)n * h->hplane : nullptr;
       launch_step<T, true>(h, s, a);
@@ -1052,7 +1109,14 @@ int do_forward_batch(sg_handle* h, int b0, int cnt, bool store_full_hist_ckpt_mo
     }));
     return SG_OK;
   }
-  if (h->recon == SG_RECON_FULL) {
+  if (h->recon == SG_RECON_BOUNDARY) {
+    SG_TRY(run_graph(h, "fwd_band/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
+      FwdPlan p;
+      p.band_save = true;
+      SG_TRY(enq_forward<T>(h, s, cnt, 0, nt, p));
+      return SG_OK;
+    }));
+  } else if (h->recon == SG_RECON_FULL) {
     SG_TRY(run_graph(h, "fwd_full/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
       FwdPlan p;
       p.hist = main_hist(h, 0);
@@ -1091,6 +1155,26 @@ int do_adjoint_batch(sg_handle* h, int cnt, const void* cached_hist, int64_t cac
       AdjPlan p;
       p.hist = hr;
       SG_TRY(enq_adjoint<T>(h, s, cnt, nt, 0, p));
+      return SG_OK;
+    }));
+    return SG_OK;
+  }
+  if (h->recon == SG_RECON_BOUNDARY) {
+    // the forward left (u_nt, inc_nt) in ({u0,u1}[nt & 1], inc): step back to
+    // u_{nt-1}, then the fused reverse-forward + adjoint sweep
+    SG_TRY(run_graph(h, "adj_band/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
+      const int fin = nt & 1;
+      void* F[2] = {h->u0, h->u1};
+      dim3 grid(cdiv(h->nxp, 128), h->nzp, cnt);
+      k_band_init<T><<<grid, 128, 0, s>>>(field<T>(F[fin], h), field<T>(h->inc, h),
+                                          field<T>(F[fin ^ 1], h),
+                                          reinterpret_cast<const T*>(h->band),
+                                          (int64_t)nt * h->bgeo.nb, nt - 1, h->bgeo, h->plane);
+      count_launch();
+      AdjPlan ap;
+      ap.band_recon = true;
+      ap.rcur0 = fin ^ 1;
+      SG_TRY(enq_adjoint<T>(h, s, cnt, nt, 0, ap));
       return SG_OK;
     }));
     return SG_OK;
@@ -1309,13 +1393,16 @@ int born_forward_t(sg_handle* h, int shot0, int count, const void* m_r, void* ou
         // The background keeps its whole history (FULL) or its checkpoints
         // (CHECKPOINT) for a following LSRTM adjoint, which then needs no
         // background re-run (4 stencil sweeps per LSRTM gradient).
+        // BOUNDARY: the background stores its sponge frame, handing a0_n to
+        // the scattered step through the one-slot history.
         const bool full = h->recon == SG_RECON_FULL;
         int cb = 0, cs = 0;  // ping-pong positions of the background / scattered fields
         for (int n = 0; n < nt; ++n) {
           FwdPlan bg;
           bg.gathers = false;
           bg.hist = main_hist(h, full ? 0 : n);
-          bg.ckpt_save = !full;
+          bg.ckpt_save = h->recon == SG_RECON_CHECKPOINT;
+          bg.band_save = h->recon == SG_RECON_BOUNDARY;
           SG_TRY(enq_forward<T>(h, s, cnt, n, n + 1, bg, &cb));
           FwdPlan sc;
           sc.point = false;
@@ -1380,10 +1467,13 @@ int born_adjoint_core(sg_handle* h, int shot0, int count, const void* data, int 
     } else {
       SG_TRY(load_batch_sources(h, b0, cnt));
       SG_TRY(zero_fields(h, true, false, cnt));
-      SG_TRY(run_graph(h, "born_bg_ckpt/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
+      const bool bnd = h->recon == SG_RECON_BOUNDARY;
+      SG_TRY(run_graph(h, (bnd ? "born_bg_band/" : "born_bg_ckpt/") + std::to_string(cnt),
+                       [&](cudaStream_t s) -> int {
         FwdPlan p;
         p.gathers = false;
-        p.ckpt_save = true;
+        p.ckpt_save = !bnd;
+        p.band_save = bnd;
         SG_TRY(enq_forward<T>(h, s, cnt, 0, nt, p));
         return SG_OK;
       }));
@@ -1456,13 +1546,30 @@ int time_kernel_t(sg_handle* h, int which, int count, int reps, float* ms) {
   count = std::min(count, h->B);
   if (which == 0 && h->recon != SG_RECON_FULL && h->hist_steps < 1)
     return fail(SG_ERR_STATE, "no history buffer");
+  if ((which == 5 || which == 6) && h->recon != SG_RECON_BOUNDARY)
+    return fail(SG_ERR_STATE, "band kernels need recon = BOUNDARY");
   SG_TRY(load_batch_sources(h, 0, count));
   cudaEvent_t e0, e1;
   SG_CK(cudaEventCreate(&e0));
   SG_CK(cudaEventCreate(&e1));
   const int n = h->d.nt / 2;
   auto body = [&](cudaStream_t s) -> int {
-    if (which == 3 || which == 4) {
+    if (which == 5 || which == 6) {
+      // band kernels walk the band store like a sweep (a different slot per launch)
+      for (int r = 0; r < reps; ++r) {
+        const int m = h->d.nt - 1 - r % (h->d.nt - 1);
+        if (which == 6) {
+          FwdPlan p;
+          p.band_save = true;
+          SG_TRY(enq_forward<T>(h, s, count, m, m + 1, p));
+        } else {
+          AdjPlan p;
+          p.band_recon = true;
+          p.rcur0 = r & 1;
+          SG_TRY(enq_adjoint<T>(h, s, count, m + 1, m, p));
+        }
+      }
+    } else if (which == 3 || which == 4) {
       // two-step launches (two time steps each); history rotates through the buffer
       HistRef hr = main_hist(h, n);
       hr.rotate = true;
@@ -1537,7 +1644,7 @@ int sg_create(const sg_desc* d, sg_handle** out) {
   if (d->dtype != SG_F32 && d->dtype != SG_F64) return fail(SG_ERR_ARG, "dtype must be 4 or 8");
   if (d->order != 2 && d->order != 8) return fail(SG_ERR_ARG, "order must be 2 or 8");
   if (!(d->dx > 0 && d->dz > 0 && d->dt > 0)) return fail(SG_ERR_ARG, "spacings must be positive");
-  if (d->recon < 0 || d->recon > 2) return fail(SG_ERR_ARG, "bad recon mode");
+  if (d->recon < 0 || d->recon > 3) return fail(SG_ERR_ARG, "bad recon mode");
   SG_CK(cudaSetDevice(d->device));
   sg_handle* h = new sg_handle();
   h->d = *d;
@@ -1605,6 +1712,26 @@ int sg_set_sponge(sg_handle* h, const double* pz, const double* px) {
   std::vector<double> x(h->ldx + 2 * kGuard + kSlack, 0.0);
   for (int i = 0; i < h->nzp; ++i) z[kGuard + i] = pz[i];
   for (int j = 0; j < h->nxp; ++j) x[kGuard + j] = px[j];
+  // frame of the band store: every row/column whose profile (in the device
+  // dtype) is below 1 at either end, i.e. every cell with damp < 1
+  auto below1 = [&](double v) { return h->esz == 4 ? (float)v < 1.0f : v < 1.0; };
+  auto frame = [&](const double* p, int n, int& lo, int& hi) {
+    lo = 0;
+    hi = 0;
+    for (int i = 0; i < (n + 1) / 2; ++i)
+      if (below1(p[i])) lo = i + 1;
+    for (int i = n - 1; i >= (n + 1) / 2; --i)
+      if (below1(p[i])) hi = n - i;
+    hi = std::min(hi, n - lo);
+  };
+  BandGeo& g = h->bgeo;
+  frame(pz, h->nzp, g.bT, g.bB);
+  frame(px, h->nxp, g.bL, g.bR);
+  g.nzp = h->nzp;
+  g.nxp = h->nxp;
+  g.ldx = h->ldx;
+  g.nb = (g.bT + g.bB) * h->nxp + (h->nzp - g.bT - g.bB) * (g.bL + g.bR);
+  free_batch(h);  // batch buffers are sized with the frame
   dfree(&h->pz_buf);
   dfree(&h->px_buf);
   if (h->esz == 4) {

@@ -114,7 +114,7 @@ def _torch():
 
 
 _RECON = {"full": _lib.SG_RECON_FULL, "checkpoint": _lib.SG_RECON_CHECKPOINT,
-          "auto": _lib.SG_RECON_AUTO}
+          "auto": _lib.SG_RECON_AUTO, "boundary": _lib.SG_RECON_BOUNDARY}
 
 
 def torch_dtype(dtype):
@@ -332,7 +332,7 @@ class Propagator:
     def query(self):
         b, r, by = C.c_int32(), C.c_int32(), C.c_double()
         _lib.check(self.lib.sg_query(self.h, C.byref(b), C.byref(r), C.byref(by)), "query")
-        return dict(batch=b.value, recon={0: "full", 1: "checkpoint"}.get(r.value, r.value),
+        return dict(batch=b.value, recon={0: "full", 1: "checkpoint", 3: "boundary"}.get(r.value, r.value),
                     device_bytes=by.value)
 
     def time_step_kernel(self, which, count=None, reps=50):

@@ -79,6 +79,57 @@ def test_reconstruction_modes_bitwise(recon):
     assert torch.equal(g0, g1)
 
 
+@pytest.mark.parametrize("order", [2, 8])
+@pytest.mark.parametrize("damp_top", [True, False])
+def test_boundary_reconstruction_fp64(order, damp_top):
+    """Boundary saving (sponge frame stored, interior run backwards inside the
+    adjoint step) reproduces the reference gradient, Born adjoint and
+    lock-step LSRTM gradient in fp64."""
+    _, wavesim = _api()
+    case = small_case(order, damp_top)
+    g = case["gold"]
+    p = wavesim.Propagator(case["grid"], case["geometry"], case["wavelet"], case["config"],
+                           dtype="float64", recon="boundary")
+    p.set_model(g["m"])
+    val, grad = p.gradient(g["obs"])
+    assert p.query()["recon"] == "boundary"
+    assert abs(val - float(g["value"])) <= F64 * abs(float(g["value"]))
+    assert rel(grad.cpu().numpy(), g["grad"]) <= F64
+    assert rel(p.born_adjoint(g["y"]).cpu().numpy(), g["img"]) <= F64
+    lv, lg = p.lsrtm_gradient(g["m_r"] * 0.5, g["born"])
+    assert abs(lv - float(g["lsrtm_value"])) <= F64 * abs(float(g["lsrtm_value"]))
+    assert rel(lg.cpu().numpy(), g["lsrtm_grad"]) <= F64
+    assert rel(p.born_forward(g["m_r"]).cpu().numpy(), g["born"]) <= F64
+    # the forward-only paths are unaffected by the reconstruction mode
+    assert rel(p.synthetic().cpu().numpy(), g["syn"]) <= F64
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_boundary_reconstruction_c1_batches(dtype):
+    """C1 (8th order): boundary reconstruction in several shot batches vs the
+    stored-history gradient and the reference golden."""
+    _, wavesim = _api()
+    case = c1(8)
+    g = case["gold"]
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    st = oracle_setup(g["m_true"], grid, geom, cfg)
+    obs = np.stack(oracle.fwi_synthetic(st, wav.samples, geom.nt, threads=5))
+    ref = wavesim.Propagator(grid, geom, wav, cfg, dtype=dtype, recon="full")
+    p = wavesim.Propagator(grid, geom, wav, cfg, dtype=dtype, recon="boundary", batch=2)
+    for q in (ref, p):
+        q.set_model(g["m_init"])
+    v0, g0 = ref.gradient(obs)
+    v1, g1 = p.gradient(obs)
+    assert p.query()["batch"] == 2
+    tol = F64 if dtype == "float64" else F32
+    assert abs(v1 - v0) <= 1e-12 * abs(v0)  # the forward is identical
+    assert rel(g1.cpu().numpy(), g0.cpu().numpy()) <= (1e-12 if dtype == "float64" else 1e-5)
+    assert rel(g1.cpu().numpy(), g["grad"]) <= tol
+    # repeated calls replay the captured graphs bit for bit
+    v2, g2 = p.gradient(obs)
+    assert v2 == v1 and torch.equal(g1, g2)
+
+
 def test_batches_match_single_launch():
     _, wavesim = _api()
     case = c1(8)
@@ -339,22 +390,39 @@ def test_aa_window_fp32_at_scale_vs_fp64_oracle():
             assert rel(step, oracle.aa_step(ref, 1.0, (gr, ar, rr))) <= 1e-6
 
 
-def test_c3_single_shot_fp32_gradient():
-    """C3 grid (201x601, 8th order, nt 4000), one shot: fp32 device gradient
-    vs the fp64 oracle."""
-    from paper_2008_11778_b200 import synthetic, wavesim
+_C3_ORACLE = {}
+
+
+def _c3_one_shot():
+    """C3 single-shot case and its fp64 oracle gradient (computed once)."""
+    from paper_2008_11778_b200 import synthetic
     from paper_2008_11778_b200.model import AcquisitionGeometry
-    case = synthetic.layered_case("c3")
-    geom0 = case["geometry"]
-    geom = AcquisitionGeometry((geom0.sources[11],), geom0.receivers, geom0.dt, geom0.nt)
+    if not _C3_ORACLE:
+        case = synthetic.layered_case("c3")
+        geom0 = case["geometry"]
+        geom = AcquisitionGeometry((geom0.sources[11],), geom0.receivers, geom0.dt, geom0.nt)
+        grid, cfg, wav = case["grid"], case["config"], case["wavelet"]
+        st_true = oracle_setup(case["true"].m, grid, geom, cfg)
+        obs = oracle.fwi_synthetic(st_true, wav.samples, geom.nt)
+        st = oracle_setup(case["init"].m, grid, geom, cfg)
+        val, grad, _ = oracle.fwi_gradient(st, obs, wav.samples, geom.nt)
+        _C3_ORACLE.update(case=case, geom=geom, obs=obs, val=val, grad=grad)
+    return _C3_ORACLE
+
+
+@pytest.mark.parametrize("recon", ["full", "boundary"])
+def test_c3_single_shot_fp32_gradient(recon):
+    """C3 grid (201x601, 8th order, nt 4000), one shot: fp32 device gradient
+    vs the fp64 oracle, with the stored history and with boundary-saving
+    reconstruction (4000 reverse steps in fp32)."""
+    from paper_2008_11778_b200 import wavesim
+    c = _c3_one_shot()
+    case, geom, obs, val, grad = c["case"], c["geom"], c["obs"], c["val"], c["grad"]
     grid, cfg, wav = case["grid"], case["config"], case["wavelet"]
-    st_true = oracle_setup(case["true"].m, grid, geom, cfg)
-    obs = oracle.fwi_synthetic(st_true, wav.samples, geom.nt)
-    st = oracle_setup(case["init"].m, grid, geom, cfg)
-    val, grad, _ = oracle.fwi_gradient(st, obs, wav.samples, geom.nt)
-    prop = wavesim.Propagator(grid, geom, wav, cfg, dtype="float32")
+    prop = wavesim.Propagator(grid, geom, wav, cfg, dtype="float32", recon=recon)
     prop.set_model(case["init"].m)
     v, g = prop.gradient(np.stack(obs))
+    assert prop.query()["recon"] == recon
     assert abs(v - val) <= F32 * val
     assert rel(g.cpu().numpy(), grad) <= F32
 

@@ -28,8 +28,9 @@ def main():
                       dtype=a.dtype, recon=a.recon, use_graphs=False)
     prop.set_model(case["init"].m)
     S = case["geometry"].n_sources
-    f = prop.time_step_kernel(0, S, a.reps)
-    b = prop.time_step_kernel(1, S, a.reps)
+    bnd = a.recon == "boundary"
+    f = prop.time_step_kernel(6 if bnd else 0, S, a.reps)
+    b = prop.time_step_kernel(5 if bnd else 1, S, a.reps)
     torch.cuda.synchronize()
     print(f"forward step {f*1e3:.1f} us, adjoint step {b*1e3:.1f} us, shots/launch "
           f"{prop.query()['batch']}")
