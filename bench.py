@@ -405,7 +405,9 @@ def run_ours(args):
     nbytes = p_host.nbytes
 
     # roofline of the dominant kernel (adjoint step + imaging), timed live with
-    # CUDA events on the launching stream
+    # CUDA events on the launching stream; the step launches run as the sweep
+    # runs them (two concurrent half-batch chains), so the time is per step of
+    # the whole batch and the bytes those of all its shots
     prop = obj.prop
     local_shots = shard.count if shard else S
     es = prop.esz
@@ -453,7 +455,7 @@ def run_ours(args):
             "config": {"workload": workload_name(args.config), "shots": S,
                        "shots_per_rank": local_shots, "nt": nt,
                        "padded_cells": C, "order": cfg.order, "recon": q["recon"],
-                       "shots_per_launch": q["batch"],
+                       "shots_per_batch": q["batch"], "chains": prop.chains(q["batch"]),
                        "l2": l2},
             "gradients_per_s": grads_per_s,
             "misfit": val,
@@ -462,9 +464,10 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved,
                          "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "shots_per_launch": launch_shots,
-                         "bytes_per_launch": dom[2], "ms_per_launch": dom[1],
-                         "forward_ms_per_launch": ms_fwd, "adjoint_ms_per_launch": ms_adj},
+                         "shots_per_step": launch_shots,
+                         "chains": prop.chains(launch_shots),
+                         "bytes_per_step": dom[2], "ms_per_step": dom[1],
+                         "forward_ms_per_step": ms_fwd, "adjoint_ms_per_step": ms_adj},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

@@ -73,7 +73,9 @@ typedef struct sg_desc {
   int32_t step_mode;                 /* 0 = auto (one step per launch), 1 = one
                                         step, 2 = two steps per launch (fp32,
                                         temporally blocked) */
-  int32_t reserved[2];
+  int32_t chains;                    /* concurrent half-batch chains per sweep:
+                                        0 = auto (2), 1 .. 4 */
+  int32_t reserved[1];
   double dx, dz, dt;                 /* metres, seconds */
   double cfl_safety;                 /* SimConfig.cfl_safety, seisopt/wavesim.py:57 */
   double mem_budget_bytes;           /* 0 = 50% of free device memory */
@@ -170,10 +172,15 @@ int sg_adjoint_history(sg_handle* h, const void* ybar_dev, void* v_dev);
 /* Diagnostics: shots per batch chosen, reconstruction mode in use, bytes held. */
 int sg_query(sg_handle* h, int32_t* batch, int32_t* recon, double* device_bytes);
 
-/* Times `reps` launches of one step kernel (0 = forward+history store,
+/* Concurrent shot chains a sweep over `count` shots runs as (desc.chains). */
+int sg_chains(sg_handle* h, int32_t count);
+
+/* Times `reps` steps of one step kernel (0 = forward+history store,
  * 1 = adjoint+imaging, 2 = forward no history; 3 / 4 = the two-step forward /
- * adjoint kernels, two time steps per launch) over `count` shots with CUDA
- * events on the handle's stream; *ms_per_launch = mean duration. */
+ * adjoint kernels, two time steps per launch; 5 / 6 = the boundary-saving
+ * reverse+adjoint and band-storing forward kernels) over `count` shots with
+ * CUDA events on the handle's stream, launched as the sweeps launch them
+ * (sg_chains concurrent chains); *ms_per_launch = mean time per step. */
 int sg_time_step_kernel(sg_handle* h, int32_t which, int32_t count, int32_t reps,
                         float* ms_per_launch);
 

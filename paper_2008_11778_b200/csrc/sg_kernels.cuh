@@ -76,6 +76,8 @@ struct StepArgs {
   int64_t plane;          // per-shot stride of field/state buffers
   int nzp, nxp, ldx, tiles_x, ntiles;
   int count, G;           // shots in this launch, shots per CTA group
+  int s0;                 // first batch shot of this launch (concurrent chains)
+  int g0;                 // first image group plane of this launch
   T dt2;
   T cz[5], cx[5];         // stencil weights k = 1..R
   int hist_on;            // FWD: store history; ADJ: image against history
@@ -403,8 +405,8 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
 
   const int tid = threadIdx.y * kTX + threadIdx.x;
   const int grp = blockIdx.y;
-  const int b0 = grp * a.G;
-  const int nb = min(a.G, a.count - b0);
+  const int b0 = a.s0 + grp * a.G;
+  const int nb = min(a.G, a.s0 + a.count - b0);
 
   if constexpr (!ADJ && (FL & FL_GATHER) != 0) {
     if ((int)blockIdx.x >= a.ntiles) {
@@ -494,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
   // (complete: the previous grid signalled its dependents only after its own
   // griddepcontrol.wait).
   T* ig = nullptr;
-  if (IMG) ig = a.image + (int64_t)grp * a.image_stride + o0;
+  if (IMG) ig = a.image + (int64_t)(a.g0 + grp) * a.image_stride + o0;
 #pragma unroll
   for (int q = 0; q < kNY; ++q) {
     if (q < nq) {

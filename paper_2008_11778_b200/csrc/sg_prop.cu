@@ -245,6 +245,9 @@ struct sg_handle {
   double cz[5] = {0}, cx[5] = {0};
   cudaStream_t stream = 0;
   cudaStream_t cap = nullptr;
+  static constexpr int kMaxChains = 4;
+  cudaStream_t chain[kMaxChains] = {};  // extra streams of concurrent shot chains (1..)
+  cudaEvent_t ev_fork = nullptr, ev_join[kMaxChains] = {};
 
   // static device data
   void* inv_m_buf = nullptr;  // plane + tail
@@ -766,7 +769,7 @@ void launch_step2_t(const sg_handle* h, cudaStream_t s, const Step2Args<T>& a, b
 // and flips after every launch (one or two steps).
 template <typename T>
 int enq_forward(sg_handle* h, cudaStream_t s, int count, int n0, int n1, const FwdPlan& p,
-                int* curp = nullptr) {
+                int* curp = nullptr, int s0 = 0) {
   void* U0 = p.fu0 ? p.fu0 : h->u0;
   void* U1 = p.fu1 ? p.fu1 : h->u1;
   const bool use2 = two_step_ok(h) && p.gsrc == nullptr && !p.band_save;
@@ -778,6 +781,7 @@ int enq_forward(sg_handle* h, cudaStream_t s, int count, int n0, int n1, const F
   StepArgs<T> a;
   SG_TRY(step_args<T>(h, a, U0, U1, S0, S1, p.hist.base, p.hist.shots * p.hist.steps));
   a.count = count;
+  a.s0 = s0;
   if (p.point) {
     a.src_rc = h->bsrc_rc;
     a.src_w = reinterpret_cast<const T*>(h->bsrc_w);
@@ -817,9 +821,12 @@ int enq_forward(sg_handle* h, cudaStream_t s, int count, int n0, int n1, const F
   int n = n0;
   while (n < n1) {
     if (p.ckpt_save && n % h->K == 0) {
+      // this launch's shots only (a chain owns planes s0 .. s0 + count - 1)
+      const size_t off = s0 ? ((size_t)h->ldx + (size_t)s0 * h->plane) * h->esz : 0;
+      const size_t len = s0 ? (size_t)count * h->plane * h->esz : pb;
       char* slot = (char*)h->ckpt + (size_t)(n / h->K) * 2 * sb;
-      cudaMemcpyAsync(slot, F[cur], pb, cudaMemcpyDeviceToDevice, s);
-      cudaMemcpyAsync(slot + sb, S[cur], pb, cudaMemcpyDeviceToDevice, s);
+      cudaMemcpyAsync(slot + off, (char*)F[cur] + off, len, cudaMemcpyDeviceToDevice, s);
+      cudaMemcpyAsync(slot + sb + off, (char*)S[cur] + off, len, cudaMemcpyDeviceToDevice, s);
     }
     const bool two = use2 && n + 1 < n1 && !(p.ckpt_save && (n + 1) % h->K == 0);
     if (two) {
@@ -861,7 +868,7 @@ struct AdjPlan {
 // `cur` flips after every launch and continues across calls of one sweep.
 template <typename T>
 int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, const AdjPlan& p,
-                int* curp = nullptr) {
+                int* curp = nullptr, int s0 = 0) {
   int cur_local = 0;
   int& cur = curp ? *curp : cur_local;
   const bool use2 = two_step_ok(h) && p.vhist == nullptr && !p.band_recon;
@@ -869,6 +876,8 @@ int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, con
   StepArgs<T> a;
   SG_TRY(step_args<T>(h, a, h->l0, h->l1, h->w, W1, p.hist.base, p.hist.shots * p.hist.steps));
   a.count = count;
+  a.s0 = s0;
+  a.g0 = s0;  // groups of the first s0 shots use at most s0 image planes
   a.ybar_stride = (int64_t)h->d.nt * h->d.n_rec;
   a.hist_on = p.hist.base != nullptr && !p.band_recon;
   a.hist_steps = p.hist.steps;
@@ -943,6 +952,51 @@ int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, con
       n -= 1;
     }
     cur ^= 1;
+  }
+  return SG_OK;
+}
+
+// ---- concurrent chains -------------------------------------------------------
+// A batch's time loop runs as independent chains over disjoint shot ranges
+// on separate streams (forked and joined inside the captured graph): every
+// step of a chain waits only for its own previous step, so one chain's launch
+// latency, pipeline fill and tail overlap the other chains' steady state.
+int nchains(const sg_handle* h, int count) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("SG_CHAINS");
+    env = e ? std::max(1, std::min(sg_handle::kMaxChains, atoi(e))) : 0;
+  }
+  // auto: two chains (measured best on B200: C3 gradient 163 -> 123 ms; three
+  // or four chains lose to the smaller per-launch batches)
+  const int want = env > 0 ? env : (h->d.chains > 0 ? h->d.chains : 2);
+  if (two_step_ok(h)) return 1;
+  return std::max(1, std::min({want, count, sg_handle::kMaxChains}));
+}
+
+template <typename F>
+int fork_chains(sg_handle* h, cudaStream_t s, int count, F&& body) {
+  const int nc = nchains(h, count);
+  if (nc == 1) return body(s, 0, count);
+  if (!h->ev_fork) {
+    SG_CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    for (int c = 1; c < sg_handle::kMaxChains; ++c) {
+      SG_CK(cudaStreamCreateWithFlags(&h->chain[c], cudaStreamNonBlocking));
+      SG_CK(cudaEventCreateWithFlags(&h->ev_join[c], cudaEventDisableTiming));
+    }
+  }
+  SG_CK(cudaEventRecord(h->ev_fork, s));
+  int s0 = 0;
+  for (int c = 0; c < nc; ++c) {
+    const int cnt = count / nc + (c < count % nc ? 1 : 0);
+    cudaStream_t cs = c == 0 ? s : h->chain[c];
+    if (c > 0) SG_CK(cudaStreamWaitEvent(cs, h->ev_fork, 0));
+    SG_TRY(body(cs, s0, cnt));
+    s0 += cnt;
+  }
+  for (int c = 1; c < nc; ++c) {
+    SG_CK(cudaEventRecord(h->ev_join[c], h->chain[c]));
+    SG_CK(cudaStreamWaitEvent(s, h->ev_join[c], 0));
   }
   return SG_OK;
 }
@@ -1103,32 +1157,36 @@ int do_forward_batch(sg_handle* h, int b0, int cnt, bool store_full_hist_ckpt_mo
   const int nt = h->d.nt;
   if (!store_full_hist_ckpt_mode) {
     SG_TRY(run_graph(h, "fwd_plain/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
-      FwdPlan p;
-      SG_TRY(enq_forward<T>(h, s, cnt, 0, nt, p));
-      return SG_OK;
+      return fork_chains(h, s, cnt, [&](cudaStream_t cs, int s0, int c) -> int {
+        FwdPlan p;
+        return enq_forward<T>(h, cs, c, 0, nt, p, nullptr, s0);
+      });
     }));
     return SG_OK;
   }
   if (h->recon == SG_RECON_BOUNDARY) {
     SG_TRY(run_graph(h, "fwd_band/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
-      FwdPlan p;
-      p.band_save = true;
-      SG_TRY(enq_forward<T>(h, s, cnt, 0, nt, p));
-      return SG_OK;
+      return fork_chains(h, s, cnt, [&](cudaStream_t cs, int s0, int c) -> int {
+        FwdPlan p;
+        p.band_save = true;
+        return enq_forward<T>(h, cs, c, 0, nt, p, nullptr, s0);
+      });
     }));
   } else if (h->recon == SG_RECON_FULL) {
     SG_TRY(run_graph(h, "fwd_full/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
-      FwdPlan p;
-      p.hist = main_hist(h, 0);
-      SG_TRY(enq_forward<T>(h, s, cnt, 0, nt, p));
-      return SG_OK;
+      return fork_chains(h, s, cnt, [&](cudaStream_t cs, int s0, int c) -> int {
+        FwdPlan p;
+        p.hist = main_hist(h, 0);
+        return enq_forward<T>(h, cs, c, 0, nt, p, nullptr, s0);
+      });
     }));
   } else {
     SG_TRY(run_graph(h, "fwd_ckpt/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
-      FwdPlan p;
-      p.ckpt_save = true;
-      SG_TRY(enq_forward<T>(h, s, cnt, 0, nt, p));
-      return SG_OK;
+      return fork_chains(h, s, cnt, [&](cudaStream_t cs, int s0, int c) -> int {
+        FwdPlan p;
+        p.ckpt_save = true;
+        return enq_forward<T>(h, cs, c, 0, nt, p, nullptr, s0);
+      });
     }));
   }
   return SG_OK;
@@ -1152,10 +1210,11 @@ int do_adjoint_batch(sg_handle* h, int cnt, const void* cached_hist, int64_t cac
     std::string key = std::string(cached_hist ? "adj_cached/" : "adj_full/") +
                       std::to_string(cnt) + "/" + std::to_string((uintptr_t)hb);
     SG_TRY(run_graph(h, key, [&](cudaStream_t s) -> int {
-      AdjPlan p;
-      p.hist = hr;
-      SG_TRY(enq_adjoint<T>(h, s, cnt, nt, 0, p));
-      return SG_OK;
+      return fork_chains(h, s, cnt, [&](cudaStream_t cs, int s0, int c) -> int {
+        AdjPlan p;
+        p.hist = hr;
+        return enq_adjoint<T>(h, cs, c, nt, 0, p, nullptr, s0);
+      });
     }));
     return SG_OK;
   }
@@ -1171,11 +1230,12 @@ int do_adjoint_batch(sg_handle* h, int cnt, const void* cached_hist, int64_t cac
                                           reinterpret_cast<const T*>(h->band),
                                           (int64_t)nt * h->bgeo.nb, nt - 1, h->bgeo, h->plane);
       count_launch();
-      AdjPlan ap;
-      ap.band_recon = true;
-      ap.rcur0 = fin ^ 1;
-      SG_TRY(enq_adjoint<T>(h, s, cnt, nt, 0, ap));
-      return SG_OK;
+      return fork_chains(h, s, cnt, [&](cudaStream_t cs, int s0, int c) -> int {
+        AdjPlan ap;
+        ap.band_recon = true;
+        ap.rcur0 = fin ^ 1;
+        return enq_adjoint<T>(h, cs, c, nt, 0, ap, nullptr, s0);
+      });
     }));
     return SG_OK;
   }
@@ -1184,19 +1244,26 @@ int do_adjoint_batch(sg_handle* h, int cnt, const void* cached_hist, int64_t cac
     const size_t pb = span_bytes(h, cnt);
     const size_t sb = span_bytes(h, h->B);
     int acur = 0;  // adjoint ping-pong position, continues across segments
+    int acur_next = 0;
     for (int seg = h->ncp - 1; seg >= 0; --seg) {
       const int n0 = seg * h->K;
       const int n1 = std::min(nt, n0 + h->K);
       char* slot = (char*)h->ckpt + (size_t)seg * 2 * sb;
       cudaMemcpyAsync(h->u0, slot, pb, cudaMemcpyDeviceToDevice, s);
       cudaMemcpyAsync(h->inc, slot + sb, pb, cudaMemcpyDeviceToDevice, s);
-      FwdPlan fp;
-      fp.gathers = false;
-      fp.hist = main_hist(h, n0);
-      SG_TRY(enq_forward<T>(h, s, cnt, n0, n1, fp));
-      AdjPlan ap;
-      ap.hist = main_hist(h, n0);
-      SG_TRY(enq_adjoint<T>(h, s, cnt, n1, n0, ap, &acur));
+      SG_TRY(fork_chains(h, s, cnt, [&](cudaStream_t cs, int s0, int c) -> int {
+        FwdPlan fp;
+        fp.gathers = false;
+        fp.hist = main_hist(h, n0);
+        SG_TRY(enq_forward<T>(h, cs, c, n0, n1, fp, nullptr, s0));
+        AdjPlan ap;
+        ap.hist = main_hist(h, n0);
+        int ac = acur;  // every chain starts the segment at the same parity
+        SG_TRY(enq_adjoint<T>(h, cs, c, n1, n0, ap, &ac, s0));
+        if (s0 == 0) acur_next = ac;  // and ends it at the same one
+        return SG_OK;
+      }));
+      acur = acur_next;
     }
     return SG_OK;
   }));
@@ -1377,12 +1444,13 @@ int born_forward_t(sg_handle* h, int shot0, int count, const void* m_r, void* ou
       SG_TRY(run_graph(h, "born_fwd_cached/" + std::to_string(cnt) + "/" +
                               std::to_string((uintptr_t)base),
                        [&](cudaStream_t s) -> int {
-                         FwdPlan p;
-                         p.point = false;
-                         p.gsrc = base;
-                         p.gsrc_shot = (int64_t)nt * h->hplane;
-                         SG_TRY(enq_forward<T>(h, s, cnt, 0, nt, p));
-                         return SG_OK;
+                         return fork_chains(h, s, cnt, [&](cudaStream_t cs, int s0, int c) {
+                           FwdPlan p;
+                           p.point = false;
+                           p.gsrc = base;
+                           p.gsrc_shot = (int64_t)nt * h->hplane;
+                           return enq_forward<T>(h, cs, c, 0, nt, p, nullptr, s0);
+                         });
                        }));
     } else {
       // lock-step: background step writes a0_n into a one-slot buffer, the
@@ -1396,6 +1464,7 @@ int born_forward_t(sg_handle* h, int shot0, int count, const void* m_r, void* ou
         // BOUNDARY: the background stores its sponge frame, handing a0_n to
         // the scattered step through the one-slot history.
         const bool full = h->recon == SG_RECON_FULL;
+        return fork_chains(h, s, cnt, [&](cudaStream_t st, int s0, int c) -> int {
         int cb = 0, cs = 0;  // ping-pong positions of the background / scattered fields
         for (int n = 0; n < nt; ++n) {
           FwdPlan bg;
@@ -1403,7 +1472,7 @@ int born_forward_t(sg_handle* h, int shot0, int count, const void* m_r, void* ou
           bg.hist = main_hist(h, full ? 0 : n);
           bg.ckpt_save = h->recon == SG_RECON_CHECKPOINT;
           bg.band_save = h->recon == SG_RECON_BOUNDARY;
-          SG_TRY(enq_forward<T>(h, s, cnt, n, n + 1, bg, &cb));
+          SG_TRY(enq_forward<T>(h, st, c, n, n + 1, bg, &cb, s0));
           FwdPlan sc;
           sc.point = false;
           sc.gsrc = h->hist;
@@ -1413,9 +1482,10 @@ int born_forward_t(sg_handle* h, int shot0, int count, const void* m_r, void* ou
           sc.fu1 = h->l1;
           sc.fs0 = h->w;
           sc.fs1 = h->w2;
-          SG_TRY(enq_forward<T>(h, s, cnt, n, n + 1, sc, &cs));
+          SG_TRY(enq_forward<T>(h, st, c, n, n + 1, sc, &cs, s0));
         }
         return SG_OK;
+        });
       }));
     }
     SG_TRY(copy_gathers_out<T>(h, (char*)out + (size_t)(b0 - shot0) * gper, cnt));
@@ -1553,7 +1623,9 @@ int time_kernel_t(sg_handle* h, int which, int count, int reps, float* ms) {
   SG_CK(cudaEventCreate(&e0));
   SG_CK(cudaEventCreate(&e1));
   const int n = h->d.nt / 2;
-  auto body = [&](cudaStream_t s) -> int {
+  // the launches run as the sweeps run them: concurrent shot chains
+  // (fork_chains), so the time per repetition is the step time of the batch
+  auto chain_body = [&](cudaStream_t s, int s0, int count) -> int {
     if (which == 5 || which == 6) {
       // band kernels walk the band store like a sweep (a different slot per launch)
       for (int r = 0; r < reps; ++r) {
@@ -1561,12 +1633,12 @@ int time_kernel_t(sg_handle* h, int which, int count, int reps, float* ms) {
         if (which == 6) {
           FwdPlan p;
           p.band_save = true;
-          SG_TRY(enq_forward<T>(h, s, count, m, m + 1, p));
+          SG_TRY(enq_forward<T>(h, s, count, m, m + 1, p, nullptr, s0));
         } else {
           AdjPlan p;
           p.band_recon = true;
           p.rcur0 = r & 1;
-          SG_TRY(enq_adjoint<T>(h, s, count, m + 1, m, p));
+          SG_TRY(enq_adjoint<T>(h, s, count, m + 1, m, p, nullptr, s0));
         }
       }
     } else if (which == 3 || which == 4) {
@@ -1590,7 +1662,8 @@ int time_kernel_t(sg_handle* h, int which, int count, int reps, float* ms) {
         p.hist = main_hist(h, n);
         p.hist.rotate = true;
       }
-      for (int r = 0; r < reps; ++r) SG_TRY(enq_forward<T>(h, s, count, n + (r & 1), n + (r & 1) + 1, p));
+      for (int r = 0; r < reps; ++r)
+        SG_TRY(enq_forward<T>(h, s, count, n + (r & 1), n + (r & 1) + 1, p, nullptr, s0));
     } else {
       // walk the history like a sweep does (a different, L2-cold plane per
       // launch) so the timing includes the streaming history read
@@ -1599,11 +1672,16 @@ int time_kernel_t(sg_handle* h, int which, int count, int reps, float* ms) {
       p.hist.rotate = true;
       for (int r = 0; r < reps; ++r) {
         const int m = (int)((h->d.nt - 1 - r % h->d.nt) % std::max<int64_t>(1, h->hist_steps));
-        SG_TRY(enq_adjoint<T>(h, s, count, m + 1, m, p));
+        SG_TRY(enq_adjoint<T>(h, s, count, m + 1, m, p, nullptr, s0));
       }
     }
     return SG_OK;
   };
+  auto body = [&](cudaStream_t s) -> int {
+    if (which == 3 || which == 4) return chain_body(s, 0, count);  // two-step: one chain
+    return fork_chains(h, s, count, chain_body);
+  };
+
   SG_TRY(body(h->stream));  // warm-up
   SG_CK(cudaEventRecord(e0, h->stream));
   SG_TRY(body(h->stream));
@@ -1694,6 +1772,11 @@ int sg_destroy(sg_handle* h) {
                    (void**)&h->inj_rec, &h->inj_w, &h->born_hist};
   for (auto p : bufs) dfree(p);
   if (h->cap) cudaStreamDestroy(h->cap);
+  for (int c = 1; c < sg_handle::kMaxChains; ++c) {
+    if (h->chain[c]) cudaStreamDestroy(h->chain[c]);
+    if (h->ev_join[c]) cudaEventDestroy(h->ev_join[c]);
+  }
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   delete h;
   return SG_OK;
 }
@@ -2001,6 +2084,8 @@ int sg_query(sg_handle* h, int32_t* batch, int32_t* recon, double* bytes) {
   if (bytes) *bytes = h->held_bytes;
   return SG_OK;
 }
+
+int sg_chains(sg_handle* h, int32_t count) { return h ? nchains(h, count) : 1; }
 
 int sg_time_step_kernel(sg_handle* h, int32_t which, int32_t count, int32_t reps, float* ms) {
   SG_TRY(check_handle(h));

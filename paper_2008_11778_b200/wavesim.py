@@ -131,7 +131,7 @@ class Propagator:
 
     def __init__(self, grid, geometry, wavelet, config=SimConfig(), dtype="float64",
                  device=None, recon="auto", batch=0, checkpoint_every=0, use_graphs=True,
-                 mem_budget_bytes=0.0, group=0, step_mode=0):
+                 mem_budget_bytes=0.0, group=0, step_mode=0, chains=0):
         torch = _torch()
         self.lib = _lib.load()
         if not torch.cuda.is_available():
@@ -161,6 +161,7 @@ class Propagator:
         d.use_graphs = 1 if use_graphs else 0
         d.group = int(group)
         d.step_mode = int(step_mode)
+        d.chains = int(chains)
         d.dx, d.dz, d.dt = grid.dx, grid.dz, geometry.dt
         d.cfl_safety = config.cfl_safety
         d.mem_budget_bytes = float(mem_budget_bytes)
@@ -334,6 +335,10 @@ class Propagator:
         _lib.check(self.lib.sg_query(self.h, C.byref(b), C.byref(r), C.byref(by)), "query")
         return dict(batch=b.value, recon={0: "full", 1: "checkpoint", 3: "boundary"}.get(r.value, r.value),
                     device_bytes=by.value)
+
+    def chains(self, count=None):
+        """Concurrent shot chains a sweep over `count` shots runs as."""
+        return int(self.lib.sg_chains(self.h, int(self.n_shots if count is None else count)))
 
     def time_step_kernel(self, which, count=None, reps=50):
         ms = C.c_float()
