@@ -618,25 +618,48 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
         bi1 = vj1 ? band_index(a, ib + q, j + 1) : -1;
       };
 
-      P col[NCOL];
-#pragma unroll
-      for (int r = 0; r < NCOL; ++r) col[r] = lds2(sc + r * SW);
-      P colu[RB ? NCOL : 1];
-      if constexpr (RB) {
-#pragma unroll
-        for (int r = 0; r < NCOL; ++r) colu[r] = lds2(scu + r * SW);
-      }
       // FULL: all kNY rows and both columns valid (interior tiles) -- no
       // per-row tests, unmasked pair stores
       auto rows = [&](auto full_tag) {
         constexpr bool FULL = decltype(full_tag)::value;
-#pragma unroll
-      for (int q = 0; q < kNY; ++q) {
-        if (!FULL && q >= nq) continue;
         auto put = [&](T* p, P v) {  // store a pair (only the valid half at the edge)
           if (FULL || vj1) st2(p, v);
           else p[0] = v.lo();
         };
+        // RB pass 1: the forward run backwards on its own register window
+        // (a_n bitwise the forward's for the same u_n, then inc_n and u_{n-1};
+        // frame cells from the store); a_n is kept for the imaging in pass 2
+        P accs[RB ? kNY : 1];
+        if constexpr (RB) {
+          P colu[NCOL];
+#pragma unroll
+          for (int r = 0; r < NCOL; ++r) colu[r] = lds2(scu + r * SW);
+#pragma unroll
+          for (int q = 0; q < kNY; ++q) {
+            if (!FULL && q >= nq) continue;
+            const P acc = accel(lap2(colu, scu, q), q);
+            accs[q] = acc;
+            const P incn = lds2(sinc + q * kBX) - dt2p * acc;
+            put(rsout + q * ldx, incn);
+            P um1 = colu[q + R] - incn;
+            if (bsrc != nullptr && tile_band) {
+              int bi0, bi1;
+              band2(q, bi0, bi1);
+              T w0, w1;
+              um1.split(w0, w1);
+              if (bi0 >= 0) w0 = bsrc[bi0];
+              if (bi1 >= 0) w1 = bsrc[bi1];
+              um1 = P::make(w0, w1);
+            }
+            put(rout + q * ldx, um1);
+          }
+        }
+        P col[NCOL];
+#pragma unroll
+        for (int r = 0; r < NCOL; ++r) col[r] = lds2(sc + r * SW);
+#pragma unroll
+      for (int q = 0; q < kNY; ++q) {
+        if (!FULL && q >= nq) continue;
         const P ucs = col[q + R];
         const P sv = lds2(sst + q * kBX);
         P lp = lap2(col, sc, q);
@@ -687,24 +710,8 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
             img[2 * q + 1] -= hh.hi() * v1;
           }
           if constexpr (RB) {
-            // forward run backwards: a_n (bitwise the forward's for the same
-            // u_n), then inc_n and u_{n-1}; frame cells come from the store
-            const P acc = accel(lap2(colu, scu, q), q);
-            img[2 * q] -= acc.lo() * v0;
-            img[2 * q + 1] -= acc.hi() * v1;
-            const P incn = lds2(sinc + q * kBX) - dt2p * acc;
-            put(rsout + q * ldx, incn);
-            P um1 = colu[q + R] - incn;
-            if (bsrc != nullptr && tile_band) {
-              int bi0, bi1;
-              band2(q, bi0, bi1);
-              T w0, w1;
-              um1.split(w0, w1);
-              if (bi0 >= 0) w0 = bsrc[bi0];
-              if (bi1 >= 0) w1 = bsrc[bi1];
-              um1 = P::make(w0, w1);
-            }
-            put(rout + q * ldx, um1);
+            img[2 * q] -= accs[q].lo() * v0;
+            img[2 * q + 1] -= accs[q].hi() * v1;
           }
           if (VHIST) put(a.vhist + (int64_t)b * a.vhist_stride + o0 + q * ldx, ucs);
         }

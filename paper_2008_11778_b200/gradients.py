@@ -250,7 +250,7 @@ class FwiObjective:
 
     def __init__(self, grid, observed, wavelet, geometry, config=SimConfig(), threads=1, *,
                  dtype="float64", device=None, shard=None, recon="auto", batch=0,
-                 checkpoint_every=0):
+                 checkpoint_every=0, mem_budget_bytes=0.0, chains=0):
         self.grid = grid
         self.wavelet = wavelet
         self.geometry = geometry
@@ -259,7 +259,8 @@ class FwiObjective:
         self.counters = EvalCounters()
         self.shard = shard
         self.prop = Propagator(grid, geometry, wavelet, config, dtype=dtype, device=device,
-                               recon=recon, batch=batch, checkpoint_every=checkpoint_every)
+                               recon=recon, batch=batch, checkpoint_every=checkpoint_every,
+                               mem_budget_bytes=mem_budget_bytes, chains=chains)
         s0, cnt = self._range()
         obs = _stack(observed)
         if obs.shape[0] != geometry.n_sources:
