@@ -50,7 +50,8 @@ extern "C" {
 /* forward-wavefield reconstruction for gradients / Born adjoints */
 #define SG_RECON_FULL 0       /* whole acceleration history in HBM */
 #define SG_RECON_CHECKPOINT 1 /* state checkpoints + segment recompute (bitwise) */
-#define SG_RECON_AUTO 2       /* FULL when it fits, else (fp32) BOUNDARY when >= 8 shots
+#define SG_RECON_AUTO 2       /* FULL when it fits, else (fp32, >= 2^20 padded cells)
+                                 BOUNDARY when >= 8 shots
                                  per batch fit, else CHECKPOINT */
 #define SG_RECON_BOUNDARY 3   /* boundary saving: u on the sponge frame every step +
                                  final state; the adjoint runs the forward backwards

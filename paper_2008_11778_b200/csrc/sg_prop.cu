@@ -382,13 +382,15 @@ int ensure_batch(sg_handle* h) {
   int recon = h->d.recon;
   const double full_b = per_shot_bytes(h, SG_RECON_FULL, K, ncp);
   const double ck_b = per_shot_bytes(h, SG_RECON_CHECKPOINT, K, ncp);
-  // AUTO: the whole history when the batch fits; else (fp32) boundary saving
-  // when it still batches >= 8 shots per launch (C5: 5% faster than
-  // checkpointing, both HBM-bound); else checkpointing (least memory)
+  // AUTO: the whole history when the batch fits; else (fp32, large grids whose
+  // steps are HBM-bound) boundary saving when it still batches >= 8 shots per
+  // launch (C5: 90.0 s vs 94.6 s checkpointed); else checkpointing (least
+  // memory; C4-sized grids: 583 ms vs 686 ms with boundary saving)
   if (recon == SG_RECON_AUTO) {
     const double bd_b = per_shot_bytes(h, SG_RECON_BOUNDARY, K, ncp);
+    const bool big = (int64_t)h->nzp * h->nxp >= (1 << 20);
     if (full_b * want <= budget) recon = SG_RECON_FULL;
-    else if (h->esz == 4 && bd_b * std::min(want, 8) <= budget) recon = SG_RECON_BOUNDARY;
+    else if (h->esz == 4 && big && bd_b * std::min(want, 8) <= budget) recon = SG_RECON_BOUNDARY;
     else recon = SG_RECON_CHECKPOINT;
   }
   const double per = recon == SG_RECON_FULL       ? full_b
