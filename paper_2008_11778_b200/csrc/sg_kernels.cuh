@@ -366,13 +366,23 @@ constexpr int FL_VHIST = 4;   // ADJ: store v_n (adjoint_solve keep_v)
 constexpr int FL_GATHER = 8;  // FWD: receiver sampling blocks present
 constexpr int FL_BAND = 16;   // FWD: store u_n on the sponge frame; ADJ: reverse-
                               // reconstruct the forward and image against it
+constexpr int FL_LOCK = 32;   // FWD: lock-step Born pair in one launch -- the
+                              // background step (second field set, point source,
+                              // optional history) feeds its a0_n to the
+                              // scattered step in registers
 
-// CTAs per SM the step kernel is built for (fp32 RB stages need 77 KB smem)
+// kernels that carry two field sets per stage (RB, LOCK)
+template <bool ADJ, int FL>
+__host__ __device__ constexpr bool step_dual() {
+  return ADJ ? (FL & FL_BAND) != 0 : (FL & FL_LOCK) != 0;
+}
+
+// CTAs per SM the step kernel is built for (fp32 dual stages need 77 KB smem)
 template <typename T, bool ADJ, int FL>
 __host__ __device__ constexpr int step_min_blocks() {
-  // (fp64 RB stages are 154 KB: one CTA per SM)
-  return sizeof(T) != 4 ? ((ADJ && (FL & FL_BAND)) ? 1 : 2)
-                        : ((ADJ && (FL & FL_BAND)) ? 2 : (ADJ ? SG_ADJ_MINB : SG_FP32_MINB));
+  // (fp64 dual stages are 154 KB: one CTA per SM)
+  return sizeof(T) != 4 ? (step_dual<ADJ, FL>() ? 1 : 2)
+                        : (step_dual<ADJ, FL>() ? 2 : (ADJ ? SG_ADJ_MINB : SG_FP32_MINB));
 }
 
 // R^T y of one cell by a walk over its CSR taps (receiver bands too wide for
@@ -390,7 +400,9 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
     k_step(const __grid_constant__ StepArgs<T> a) {
   constexpr bool RB = ADJ && (FL & FL_BAND) != 0;     // fused reverse + adjoint
   constexpr bool BSAVE = !ADJ && (FL & FL_BAND) != 0;  // forward band store
-  using SM = Smem<T, R, ADJ, RB>;
+  constexpr bool LOCK = !ADJ && (FL & FL_LOCK) != 0;   // fused Born background + scattered
+  constexpr bool DUAL = RB || LOCK;                    // second field set per stage
+  using SM = Smem<T, R, ADJ, DUAL>;
   using P = V2<T>;
   constexpr int SW = SM::SW;
   constexpr int NCOL = kNY + 2 * R;  // rows of the vertical window
@@ -457,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
     T* st = sbase + s * SM::STAGE;
     const int b = b0 + k;
     constexpr uint32_t bytes =
-        RB ? (2 * SM::SW * SM::SH + 2 * SM::TILE) * (uint32_t)sizeof(T)
+        DUAL ? (2 * SM::SW * SM::SH + 2 * SM::TILE) * (uint32_t)sizeof(T)
            : (SM::SW * SM::SH + (LOAD_HIST ? 2 : 1) * SM::TILE) * (uint32_t)sizeof(T);
     mbar_expect_tx(&bar[s], bytes);
     // rows of a guarded plane: data row i lives at plane row kGuard + i
@@ -466,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
     if (LOAD_HIST)
       tma_load_3d(st + SM::HALO + SM::TILE, &a.h_tile, &bar[s], j0, i0,
                   b * a.hist_steps + a.hist_slot);
-    if (RB) {
+    if (DUAL) {
       tma_load_3d(st + SM::HALO + SM::TILE, &a.r_halo[a.rcur], &bar[s], j0 - kHalo,
                   kGuard + i0 - kHalo, b);
       tma_load_3d(st + 2 * SM::HALO + SM::TILE, &a.r_stile, &bar[s], j0, kGuard + i0, b);
@@ -546,11 +558,12 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
     T* __restrict__ rsout = nullptr;  // RB: inc_n
     const T* __restrict__ bsrc = nullptr;
     T* __restrict__ bdst = nullptr;
-    if (RB) {
+    if (DUAL) {
       rout = a.rf[a.rcur ^ 1] + sb + o0;
       rsout = a.rstate + sb + o0;
-      if (a.band_slot >= 0) bsrc = a.band + (int64_t)b * a.band_stride + (int64_t)a.band_slot * a.nb;
     }
+    if (RB && a.band_slot >= 0)
+      bsrc = a.band + (int64_t)b * a.band_stride + (int64_t)a.band_slot * a.nb;
     if (BSAVE) bdst = a.band + (int64_t)b * a.band_stride + (int64_t)a.band_slot * a.nb;
 
     mbar_wait(&bar[k % NS], (k / NS) & 1);
@@ -629,7 +642,24 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
         // RB pass 1: the forward run backwards on its own register window
         // (a_n bitwise the forward's for the same u_n, then inc_n and u_{n-1};
         // frame cells from the store); a_n is kept for the imaging in pass 2
-        P accs[RB ? kNY : 1];
+        P accs[DUAL ? kNY : 1];
+        if constexpr (LOCK) {
+          // LOCK pass 1: the background step (point source, optional history
+          // store) on its own register window; a0_n feeds pass 2
+          P colu[NCOL];
+#pragma unroll
+          for (int r = 0; r < NCOL; ++r) colu[r] = lds2(scu + r * SW);
+#pragma unroll
+          for (int q = 0; q < kNY; ++q) {
+            if (!FULL && q >= nq) continue;
+            const P acc = accel(lap2(colu, scu, q), q);
+            accs[q] = acc;
+            if (HIST) put(hout + q * ldx, acc);
+            const P so = P::fma(dt2p, acc, lds2(sinc + q * kBX)) * dd[q];
+            put(rsout + q * ldx, so);
+            put(rout + q * ldx, P::fma(dd[q], colu[q + R], so));
+          }
+        }
         if constexpr (RB) {
           P colu[NCOL];
 #pragma unroll
@@ -665,14 +695,17 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
         P lp = lap2(col, sc, q);
         if (!ADJ) {
           if (GSRC) lp = P::fma(ldg2(gin + q * ldx), ldg2(a.gscale + o0 + q * ldx), lp);
-          const P acc = accel(lp, q);
+          // LOCK: the scattered step, driven by the background's a0_n
+          // (seisopt/wavesim.py:289-290; no point source)
+          if (LOCK) lp = P::fma(accs[q], ldg2(a.gscale + o0 + q * ldx), lp);
+          const P acc = LOCK ? lp * im[q] : accel(lp, q);
           if (BSAVE && tile_band) {
             int bi0, bi1;
             band2(q, bi0, bi1);
             if (bi0 >= 0) bdst[bi0] = ucs.lo();
             if (bi1 >= 0) bdst[bi1] = ucs.hi();
           }
-          if (HIST) put(hout + q * ldx, acc);
+          if (HIST && !LOCK) put(hout + q * ldx, acc);
           const P so = P::fma(dt2p, acc, sv) * dd[q];
           put(sout + q * ldx, so);
           put(fout + q * ldx, P::fma(dd[q], ucs, so));

@@ -574,8 +574,7 @@ int step_args(sg_handle* h, StepArgs<T>& a, void* F0, void* F1, void* S0, void* 
 template <typename T, int R, bool ADJ, int FL>
 void launch_step_f(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a0) {
   static bool attr = false;
-  constexpr bool RBK = ADJ && (FL & FL_BAND) != 0;
-  constexpr int smem = step_smem_bytes<T, R, ADJ, RBK>();
+  constexpr int smem = step_smem_bytes<T, R, ADJ, step_dual<ADJ, FL>()>();
   constexpr int per_sm = step_min_blocks<T, ADJ, FL>();
   if (!attr) {
     cudaFuncSetAttribute(k_step<T, R, ADJ, FL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -611,6 +610,10 @@ void launch_step_r(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a) {
     else if (fl & FL_VHIST) launch_step_f<T, R, ADJ, FL_VHIST>(h, s, a);
     else if (fl & FL_HIST) launch_step_f<T, R, ADJ, FL_HIST>(h, s, a);
     else launch_step_f<T, R, ADJ, 0>(h, s, a);
+  } else if (a.rstate != nullptr) {
+    // fused lock-step Born pair (scattered gathers; background history optional)
+    if (fl & FL_HIST) launch_step_f<T, R, ADJ, FL_LOCK | FL_GATHER | FL_HIST>(h, s, a);
+    else launch_step_f<T, R, ADJ, FL_LOCK | FL_GATHER>(h, s, a);
   } else if (fl & FL_BAND) {
     // band-saving forwards: FWI gradient (gathers) and Born background (one-slot history)
     if (fl & FL_HIST) launch_step_f<T, R, ADJ, FL_BAND | FL_HIST>(h, s, a);
@@ -961,6 +964,60 @@ int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, con
       launch_step<T, true>(h, s, a);
       n -= 1;
     }
+    cur ^= 1;
+  }
+  return SG_OK;
+}
+
+// Lock-step Born forward over steps n0 .. n1-1 in fused launches: the
+// background (u0/u1, inc; point source; history `hist` if given; checkpoints
+// in CHECKPOINT mode) and the scattered field (l0/l1, w; source a0_n *
+// gscale; gathers) of shots [s0, s0 + count) advance together.
+template <typename T>
+int enq_lockstep(sg_handle* h, cudaStream_t s, int count, int n0, int n1, const HistRef& hist,
+                 bool ckpt_save, int s0 = 0) {
+  StepArgs<T> a;
+  SG_TRY(step_args<T>(h, a, h->l0, h->l1, h->w, h->w, hist.base, hist.shots * hist.steps));
+  if (h->d.order == 8) {
+    SG_TRY((get_map<T, 4>(h, h->u0, MAP_HALO, h->B, &a.r_halo[0])));
+    SG_TRY((get_map<T, 4>(h, h->u1, MAP_HALO, h->B, &a.r_halo[1])));
+    SG_TRY((get_map<T, 4>(h, h->inc, MAP_TILE, h->B, &a.r_stile)));
+  } else {
+    SG_TRY((get_map<T, 1>(h, h->u0, MAP_HALO, h->B, &a.r_halo[0])));
+    SG_TRY((get_map<T, 1>(h, h->u1, MAP_HALO, h->B, &a.r_halo[1])));
+    SG_TRY((get_map<T, 1>(h, h->inc, MAP_TILE, h->B, &a.r_stile)));
+  }
+  a.count = count;
+  a.s0 = s0;
+  a.rf[0] = field<T>(h->u0, h);
+  a.rf[1] = field<T>(h->u1, h);
+  a.rstate = field<T>(h->inc, h);
+  a.src_rc = h->bsrc_rc;
+  a.src_w = reinterpret_cast<const T*>(h->bsrc_w);
+  a.gscale = field<T>(h->gscale_buf, h);
+  a.hist_on = hist.base != nullptr;
+  a.hist_steps = hist.steps;
+  a.hist = reinterpret_cast<T*>(hist.base);
+  a.hplane = h->hplane;
+  a.gather_stride = (int64_t)h->d.nt * h->d.n_rec;
+  const size_t pb = span_bytes(h, count);
+  const size_t sb = span_bytes(h, h->B);
+  void* F[2] = {h->u0, h->u1};
+  int cur = 0;
+  for (int n = n0; n < n1; ++n) {
+    if (ckpt_save && n % h->K == 0) {
+      const size_t off = s0 ? ((size_t)h->ldx + (size_t)s0 * h->plane) * h->esz : 0;
+      const size_t len = s0 ? (size_t)count * h->plane * h->esz : pb;
+      char* slot = (char*)h->ckpt + (size_t)(n / h->K) * 2 * sb;
+      cudaMemcpyAsync(slot + off, (char*)F[cur] + off, len, cudaMemcpyDeviceToDevice, s);
+      cudaMemcpyAsync(slot + sb + off, (char*)h->inc + off, len, cudaMemcpyDeviceToDevice, s);
+    }
+    a.cur = cur;   // scattered and background fields flip together
+    a.rcur = cur;
+    a.amp = (T)h->wavelet[n];
+    if (a.hist_on) a.hist_slot = hist.slot(n);
+    a.gather = reinterpret_cast<T*>(h->gath) + (int64_t)n * h->d.n_rec;
+    launch_step<T, false>(h, s, a);
     cur ^= 1;
   }
   return SG_OK;
@@ -1474,6 +1531,14 @@ int born_forward_t(sg_handle* h, int shot0, int count, const void* m_r, void* ou
         // BOUNDARY: the background stores its sponge frame, handing a0_n to
         // the scattered step through the one-slot history.
         const bool full = h->recon == SG_RECON_FULL;
+        if (h->recon != SG_RECON_BOUNDARY && h->d.step_mode != 2) {
+          // one fused launch per step (a0_n stays in registers)
+          return fork_chains(h, s, cnt, [&](cudaStream_t st, int s0, int c) -> int {
+            HistRef hr;
+            if (full) hr = main_hist(h, 0);
+            return enq_lockstep<T>(h, st, c, 0, nt, hr, !full, s0);
+          });
+        }
         return fork_chains(h, s, cnt, [&](cudaStream_t st, int s0, int c) -> int {
         int cb = 0, cs = 0;  // ping-pong positions of the background / scattered fields
         for (int n = 0; n < nt; ++n) {
