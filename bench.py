@@ -486,6 +486,9 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved,
                          "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         # ncu DRAM bytes of the step / its live time: the HBM
+                         # actually moved (C3 fields stay in L2, so < achieved)
+                         "traffic_gbs": (traffic / (dom[1] / 1e3) / 1e9) if traffic else None,
                          "shots_per_step": launch_shots,
                          "chains": prop.chains(launch_shots),
                          "bytes_per_step": dom[2], "ms_per_step": dom[1],
