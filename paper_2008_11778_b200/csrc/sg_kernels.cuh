@@ -38,8 +38,12 @@ namespace sg {
 
 constexpr int kGuard = 4;         // zero guard rows above/below each plane
 constexpr int kTileRowsMax = 64;  // tail padding covers tiles up to this height
-// 64 x 32 tile, 256 threads = 32 column pairs x 8 row groups of kNY rows
-constexpr int kBX = 64, kTX = 32, kTY = 8, kNY = 4, kTH = kTY * kNY;
+// 64 x (8 kNY) tile, 256 threads = 32 column pairs x 8 row groups of kNY rows
+#ifndef SG_NY
+#define SG_NY 4
+#endif
+constexpr int kBX = 64, kTX = 32, kTY = 8, kNY = SG_NY, kTH = kTY * kNY;
+constexpr int kTH2 = 32;  // tile height of the two-step kernel (sg_kernels2.cuh)
 constexpr int kThreads = kTX * kTY;
 // TMA halo boxes are always kHalo wide (the 8th-order radius); the 2nd-order
 // stencil reads the inner ring only.  72 x 40 boxes keep every TMA row a

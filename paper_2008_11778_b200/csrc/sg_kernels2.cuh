@@ -28,9 +28,9 @@ namespace sg {
 
 constexpr int kE = kHalo;             // ring width of step 1 (= 8th-order radius)
 constexpr int kEW = kBX + 2 * kE;     // 72: step-1 region width
-constexpr int kEH = kTH + 2 * kE;     // 40: step-1 region height
+constexpr int kEH = kTH2 + 2 * kE;     // 40: step-1 region height
 constexpr int kUW = kBX + 4 * kE;     // 80: field box width
-constexpr int kUH = kTH + 4 * kE;     // 48: field box height
+constexpr int kUH = kTH2 + 4 * kE;     // 48: field box height
 constexpr int kTY2 = 4;               // thread rows; block = kEW x kTY2 = 288 threads
 constexpr int kNY1 = kEH / kTY2;      // 10 step-1 rows per thread
 constexpr int kThreads2 = kEW * kTY2;
@@ -82,7 +82,7 @@ template <bool ADJ>
 struct Smem2 {
   static constexpr int U = kUW * kUH;        // 3840
   static constexpr int S = kEW * kEH;        // 2880
-  static constexpr int H = ADJ ? 2 * kBX * kTH : 0;
+  static constexpr int H = ADJ ? 2 * kBX * kTH2 : 0;
   static constexpr int STAGE = U + S + H;
   static constexpr int IM = kEW * kEH;
   static constexpr int MID = kEW * kEH;
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kThreads2, 2) k_step2(const __grid_constant__ 
   const int nb = min(a.G, a.count - b0);
   const int tile = blockIdx.x;
   const int tzi = tile / a.tiles_x;
-  const int i0 = tzi * kTH;
+  const int i0 = tzi * kTH2;
   const int j0 = (tile - tzi * a.tiles_x) * kBX;
 
   if (tid == 0) {
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kThreads2, 2) k_step2(const __grid_constant__ 
     tma_load_3d(st + SM::U, &a.s_ring[a.cur], &bar[s], j0 - kE, kGuard + i0 - kE, b);
     if (ADJ && HIST) {
       tma_load_3d(st + SM::U + SM::S, &a.h_tile, &bar[s], j0, i0, b * a.hist_steps + a.slot0);
-      tma_load_3d(st + SM::U + SM::S + kBX * kTH, &a.h_tile, &bar[s], j0, i0,
+      tma_load_3d(st + SM::U + SM::S + kBX * kTH2, &a.h_tile, &bar[s], j0, i0,
                   b * a.hist_steps + a.slot1);
     }
   };
@@ -170,10 +170,10 @@ __global__ void __launch_bounds__(kThreads2, 2) k_step2(const __grid_constant__ 
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const int r = a.src_rc[(b * 4 + t) * 2], c = a.src_rc[(b * 4 + t) * 2 + 1];
-        src_here |= (r >= i0 - kE && r < i0 + kTH + kE && c >= j0 - kE && c < j0 + kBX + kE);
+        src_here |= (r >= i0 - kE && r < i0 + kTH2 + kE && c >= j0 - kE && c < j0 + kBX + kE);
       }
     }
-    const bool inj_tile = ADJ && a.ybar != nullptr && a.inj_row0 < i0 + kTH + kE &&
+    const bool inj_tile = ADJ && a.ybar != nullptr && a.inj_row0 < i0 + kTH2 + kE &&
                           a.inj_row0 + a.inj_nrows > i0 - kE;
     mbar_wait(&bar[k & 1], (k >> 1) & 1);
     const T* su = sbase + (k & 1) * SM::STAGE;
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kThreads2, 2) k_step2(const __grid_constant__ 
                 if (r == gi && c == gj) acc += a.amp0 * a.src_w[b * 4 + t] * im[q2];
               }
             }
-            const bool in_tile = col_in_tile && (er0 + q2) >= kE && (er0 + q2) < kE + kTH;
+            const bool in_tile = col_in_tile && (er0 + q2) >= kE && (er0 + q2) < kE + kTH2;
             if (HIST && in_tile && gi < a.nzp && gj < a.nxp)
               a.hist[((int64_t)b * a.hist_steps + a.slot0) * a.hplane + gi * a.ldx + gj] = acc;
             s1[q2] = dd[q2] * (sv + a.dt2 * acc);
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kThreads2, 2) k_step2(const __grid_constant__ 
             }
             s1[q2] = dd[q2] * sv + lp;
             v1[q2] = dd[q2] * ucs[h] + (a.dt2 * im[q2] * dd[q2]) * s1[q2];
-            const bool in_tile = col_in_tile && (er0 + q2) >= kE && (er0 + q2) < kE + kTH;
+            const bool in_tile = col_in_tile && (er0 + q2) >= kE && (er0 + q2) < kE + kTH2;
             if (HIST && in_tile) {
               const int ti = er0 + q2 - kE, tj = ex - kE;
               img[q2] -= su[SM::U + SM::S + ti * kBX + tj] * ucs[h];
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kThreads2, 2) k_step2(const __grid_constant__ 
 #pragma unroll
       for (int q = 0; q < kNY1; ++q) {
         const int er = er0 + q;
-        if (er < kE || er >= kE + kTH) continue;  // ring rows: step 1 only
+        if (er < kE || er >= kE + kTH2) continue;  // ring rows: step 1 only
         const int gi = gi0 + q;
         if (gi >= a.nzp || gj >= a.nxp) continue;
         const T uc = v1[q];
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kThreads2, 2) k_step2(const __grid_constant__ 
           fout[o] = dd[q] * uc + (a.dt2 * im[q] * dd[q]) * so;
           if (HIST) {
             const int ti = er - kE, tj = ex - kE;
-            img[q] -= su[SM::U + SM::S + kBX * kTH + ti * kBX + tj] * uc;
+            img[q] -= su[SM::U + SM::S + kBX * kTH2 + ti * kBX + tj] * uc;
           }
         }
       }
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kThreads2, 2) k_step2(const __grid_constant__ 
 #pragma unroll
     for (int q = 0; q < kNY1; ++q) {
       const int er = er0 + q, gi = gi0 + q;
-      if (er >= kE && er < kE + kTH && gi < a.nzp && gj < a.nxp) ig[gi * a.ldx + gj] += img[q];
+      if (er >= kE && er < kE + kTH2 && gi < a.nzp && gj < a.nxp) ig[gi * a.ldx + gj] += img[q];
     }
   }
 }

@@ -35,7 +35,8 @@ using namespace sg;
 
 namespace {
 
-constexpr int BX = kBX, TH = kTH;  // 64 x 32 tiles, 256 threads
+constexpr int BX = kBX, TH = kTH;  // one-step kernel tiles (64 x kTH), 256 threads
+constexpr int TH2 = kTH2;          // two-step kernel tile height
 constexpr int RB = kThreads;        // threads per block
 constexpr int kSlack = 256;         // column slack for profile arrays
 
@@ -242,6 +243,7 @@ struct sg_handle {
   int64_t hplane = 0;  // compact-row history plane nzp*ldx
   int64_t tail = 0;    // slack after the last plane of a batch buffer
   int tiles_x = 0, ntiles = 0, rec_blocks = 0;
+  int ntiles2 = 0;  // tiles of the two-step kernel (64 x kTH2)
   double cz[5] = {0}, cx[5] = {0};
   cudaStream_t stream = 0;
   cudaStream_t cap = nullptr;
@@ -475,7 +477,8 @@ int ngroups(const sg_handle* h, int count, int per_sm = 0) {
 // TMA descriptors.  Guarded buffers (fields, state) are viewed as 3-D
 // {ldx, nzp + 2 kGuard, B} starting after the lead row; histories as
 // {ldx, nzp, planes}.  Out-of-bounds boxes read as zero and are clipped on store.
-enum MapKind { MAP_HALO = 0, MAP_TILE = 1, MAP_HIST = 2, MAP_HALO2 = 3, MAP_RING = 4 };
+enum MapKind { MAP_HALO = 0, MAP_TILE = 1, MAP_HIST = 2, MAP_HALO2 = 3, MAP_RING = 4,
+               MAP_HIST2 = 5 };
 
 template <typename T, int R>
 int get_map(sg_handle* h, void* base, int kind, int64_t planes, CUtensorMap* out) {
@@ -489,15 +492,21 @@ int get_map(sg_handle* h, void* base, int kind, int64_t planes, CUtensorMap* out
   }
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(SG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  const int rows = (kind == MAP_HIST) ? h->nzp : h->nzp + 2 * kGuard;
-  const int64_t pl = (kind == MAP_HIST) ? h->hplane : h->plane;
-  void* g = (kind == MAP_HIST) ? base : (void*)((char*)base + (size_t)h->ldx * sizeof(T));
+  const bool hk = kind == MAP_HIST || kind == MAP_HIST2;
+  const int rows = hk ? h->nzp : h->nzp + 2 * kGuard;
+  const int64_t pl = hk ? h->hplane : h->plane;
+  void* g = hk ? base : (void*)((char*)base + (size_t)h->ldx * sizeof(T));
   cuuint64_t dims[3] = {(cuuint64_t)h->ldx, (cuuint64_t)rows, (cuuint64_t)planes};
   cuuint64_t strides[2] = {(cuuint64_t)h->ldx * sizeof(T), (cuuint64_t)pl * sizeof(T)};
   cuuint32_t bw = BX, bh = TH;
-  if (kind == MAP_HALO || kind == MAP_RING) {
+  if (kind == MAP_HALO) {
     bw = BX + 2 * kHalo;
     bh = TH + 2 * kHalo;
+  } else if (kind == MAP_RING) {
+    bw = kEW;
+    bh = kEH;
+  } else if (kind == MAP_HIST2) {
+    bh = TH2;
   } else if (kind == MAP_HALO2) {
     bw = kUW;
     bh = kUH;
@@ -690,7 +699,7 @@ int step2_args(sg_handle* h, Step2Args<T>& a, void* F0, void* F1, void* S0, void
   SG_TRY((get_map<T, 4>(h, S0, MAP_RING, h->B, &a.s_ring[0])));
   SG_TRY((get_map<T, 4>(h, S1, MAP_RING, h->B, &a.s_ring[1])));
   SG_TRY((get_map<T, 4>(h, h->inv_m_buf, MAP_RING, 1, &a.m_ring[0])));
-  if (hist) SG_TRY((get_map<T, 4>(h, hist, MAP_HIST, hist_planes, &a.h_tile)));
+  if (hist) SG_TRY((get_map<T, 4>(h, hist, MAP_HIST2, hist_planes, &a.h_tile)));
   a.f[0] = field<T>(F0, h);
   a.f[1] = field<T>(F1, h);
   a.state[0] = field<T>(S0, h);
@@ -702,7 +711,7 @@ int step2_args(sg_handle* h, Step2Args<T>& a, void* F0, void* F1, void* S0, void
   a.nxp = h->nxp;
   a.ldx = h->ldx;
   a.tiles_x = h->tiles_x;
-  a.ntiles = h->ntiles;
+  a.ntiles = h->ntiles2;
   a.dt2 = (T)(h->d.dt * h->d.dt);
   for (int k = 0; k < 5; ++k) {
     a.cz[k] = (T)h->cz[k];
@@ -729,7 +738,7 @@ int group2_for(const sg_handle* h, int count) {
   int best = 1;
   double best_cost = 1e300;
   for (int G = 1; G <= std::min(8, count); ++G) {
-    const int64_t items = (int64_t)h->ntiles * ((count + G - 1) / G);
+    const int64_t items = (int64_t)h->ntiles2 * ((count + G - 1) / G);
     const double rounds = (double)((items + slots - 1) / slots);
     const double cost = rounds * G * (1.0 + 0.6 / G);
     if (cost < best_cost - 1e-9) {
@@ -749,7 +758,7 @@ void launch_step2_f(const sg_handle* h, cudaStream_t s, const Step2Args<float>& 
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  dim3 grid(h->ntiles, (a.count + a.G - 1) / a.G), block(kEW, kTY2);
+  dim3 grid(h->ntiles2, (a.count + a.G - 1) / a.G), block(kEW, kTY2);
   k_step2<R, ADJ, HIST, GATHER><<<grid, block, smem, s>>>(a);
   count_launch();
 }
@@ -1811,6 +1820,7 @@ int sg_create(const sg_desc* d, sg_handle** out) {
   h->tail = (int64_t)(kTileRowsMax + 2 * kGuard + 4) * h->ldx;
   h->tiles_x = (h->nxp + BX - 1) / BX;
   h->ntiles = h->tiles_x * ((h->nzp + TH - 1) / TH);
+  h->ntiles2 = h->tiles_x * ((h->nzp + TH2 - 1) / TH2);
   h->rec_blocks = (d->n_rec + RB - 1) / RB;
   cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, d->device);
   {
@@ -1948,14 +1958,14 @@ int sg_set_geometry(sg_handle* h, const int32_t* src_rows, const int32_t* src_co
     iw[at] = rec_w[e];
   }
   // receivers grouped by the tile of their first tap (two-step forward)
-  std::vector<int> rrc(8 * R), tcount(h->ntiles + 1, 0), trec(R);
+  std::vector<int> rrc(8 * R), tcount(h->ntiles2 + 1, 0), trec(R);
   for (int e = 0; e < 4 * R; ++e) {
     rrc[2 * e] = rec_rows[e];
     rrc[2 * e + 1] = rec_cols[e];
   }
-  auto tile_of = [&](int r) { return (rec_rows[r] / TH) * h->tiles_x + rec_cols[r] / BX; };
+  auto tile_of = [&](int r) { return (rec_rows[r] / TH2) * h->tiles_x + rec_cols[r] / BX; };
   for (int r = 0; r < R; ++r) tcount[tile_of(r) + 1]++;
-  for (int t = 0; t < h->ntiles; ++t) tcount[t + 1] += tcount[t];
+  for (int t = 0; t < h->ntiles2; ++t) tcount[t + 1] += tcount[t];
   {
     std::vector<int> fill(tcount.begin(), tcount.end() - 1);
     for (int r = 0; r < R; ++r) trec[fill[tile_of(r)]++] = r;
