@@ -445,8 +445,10 @@ def run_ours(args):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            tr = json.load(open(tpath))
-            traffic = tr.get(args.config, {}).get(dom[0])
+            tr = json.load(open(tpath)).get(args.config, {})
+            traffic = tr.get(dom[0])
+            if traffic is not None and tr.get("per_shot"):
+                traffic *= launch_shots
         except Exception:
             traffic = None
 
