@@ -529,6 +529,32 @@ def test_c1_fp32_aa_misfit_curve():
     assert np.max(np.abs(mine - ref) / ref) <= 0.01
 
 
+def test_c3_fp32_aa_misfit_curve_vs_fp64():
+    """C3 production path (201x601, 8th order, nt 4000; 10 of the 30 shots to
+    bound the fp64 run): 20 device-resident AA(m=10) iterations in fp32 stay
+    within 1 % of the fp64 run's misfit curve (fp64 = the reference to 1e-12,
+    test_c1_fp64_gradient), with the same accepted blend steps."""
+    from paper_2008_11778_b200 import anderson, gradients, synthetic
+    case = synthetic.layered_case("c3", n_shots=10)
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    from paper_2008_11778_b200.wavesim import Propagator
+    prop = Propagator(grid, geom, wav, cfg, dtype="float64")
+    prop.set_model(case["true"].m)
+    obs = prop.synthetic().cpu().numpy()
+    prop.close()
+    curves = {}
+    for dtype in ("float64", "float32"):
+        obj = gradients.FwiObjective(grid, obs, wav, geom, cfg, dtype=dtype)
+        res = anderson.minimize_aa(obj, case["init"].m.ravel(), memory=10, max_iters=20)
+        curves[dtype] = np.array([[r.objective, r.step] for r in res.report.rows])
+        obj.prop.close()
+    ref, mine = curves["float64"], curves["float32"]
+    assert mine.shape == ref.shape == (21, 2)
+    assert ref[-1, 0] < 0.05 * ref[0, 0]  # the run actually converges
+    assert np.max(np.abs(mine[:, 0] - ref[:, 0]) / ref[:, 0]) <= 0.01
+    assert np.array_equal(mine[:, 1], ref[:, 1])
+
+
 @pytest.mark.parametrize("order", [2, 8])
 @pytest.mark.parametrize("recon", ["full", "checkpoint"])
 def test_two_step_kernel_matches_one_step(order, recon):
