@@ -77,7 +77,12 @@ typedef struct sg_desc {
                                         temporally blocked) */
   int32_t chains;                    /* concurrent half-batch chains per sweep:
                                         0 = auto (2), 1 .. 4 */
-  int32_t reserved[1];
+  int32_t resident;                  /* fp32 cluster-resident whole-sweep kernels
+                                        (one thread-block cluster per shot, field
+                                        in shared memory, one launch per sweep) for
+                                        grids that fit: 1 = on; 0 = auto and -1 =
+                                        off both use the one-step kernels (the
+                                        resident ones measured slower on B200) */
   double dx, dz, dt;                 /* metres, seconds */
   double cfl_safety;                 /* SimConfig.cfl_safety, seisopt/wavesim.py:57 */
   double mem_budget_bytes;           /* 0 = 50% of free device memory */
@@ -176,6 +181,11 @@ int sg_query(sg_handle* h, int32_t* batch, int32_t* recon, double* device_bytes)
 
 /* Concurrent shot chains a sweep over `count` shots runs as (desc.chains). */
 int sg_chains(sg_handle* h, int32_t count);
+
+/* Cluster-resident sweep plan (desc.resident): out[6] = {in use (0/1), CTAs per
+ * cluster, padded columns per CTA, threads per CTA, clusters resident at once,
+ * adjoint shared-memory bytes per CTA}.  Plans on first use. */
+int sg_resident_plan(sg_handle* h, int32_t* out);
 
 /* Times `reps` steps of one step kernel (0 = forward+history store,
  * 1 = adjoint+imaging, 2 = forward no history; 3 / 4 = the two-step forward /

@@ -43,7 +43,7 @@ class SgDesc(C.Structure):
         ("dtype", C.c_int32), ("order", C.c_int32), ("recon", C.c_int32),
         ("batch", C.c_int32), ("checkpoint_every", C.c_int32), ("device", C.c_int32),
         ("use_graphs", C.c_int32), ("group", C.c_int32), ("step_mode", C.c_int32),
-        ("chains", C.c_int32), ("reserved", C.c_int32 * 1),
+        ("chains", C.c_int32), ("resident", C.c_int32),
         ("dx", C.c_double), ("dz", C.c_double), ("dt", C.c_double),
         ("cfl_safety", C.c_double), ("mem_budget_bytes", C.c_double),
     ]
@@ -79,6 +79,7 @@ SIGNATURES = {
     "sg_adjoint_history": (C.c_int, [_P, _P, _P]),
     "sg_query": (C.c_int, [_P, _IP, _IP, _DP]),
     "sg_chains": (C.c_int, [_P, C.c_int32]),
+    "sg_resident_plan": (C.c_int, [_P, _IP]),
     "sg_time_step_kernel": (C.c_int, [_P, _I32, _I32, _I32, C.POINTER(C.c_float)]),
     "sg_launch_count": (C.c_int64, []),
     "sg_aa_create": (C.c_int, [_I64, _I32, _I32, _I32, C.POINTER(_P)]),

@@ -25,6 +25,7 @@
 #include "sg_common.cuh"
 #include "sg_kernels.cuh"
 #include "sg_kernels2.cuh"
+#include "sg_resident.cuh"
 
 namespace sg {
 thread_local std::string g_err;
@@ -303,6 +304,14 @@ struct sg_handle {
   int born_b0 = -1, born_count = 0;
 
   std::map<std::string, GraphEntry> graphs;
+
+  // cluster-resident whole-sweep kernels (sg_resident.cuh)
+  std::vector<int> rec_rows_h, rec_cols_h;  // receiver taps (4, n_rec), host copy
+  void* wav_dev = nullptr;                  // wavelet amplitudes in the device dtype
+  int res_state = 0;                        // 0 = not planned, 1 = usable, -1 = unavailable
+  int res_CL = 0, res_W = 0, res_Q = 0, res_runs = 0, res_SW = 0, res_SR = 0;
+  int res_hrows = 0, res_hboxes = 0, res_threads = 0, res_clusters = 0;
+  int* res_rec = nullptr;  // rec_off (4 n_rec) | rec_list (n_rec) | rec_start (CL + 1)
 };
 
 namespace {
@@ -349,6 +358,8 @@ void free_batch(sg_handle* h) {
                    &h->l1, &h->w, &h->w2, &h->gath, &h->inj_dense, &h->hist, &h->ckpt, &h->band, &h->img, &h->acc_img,
                    (void**)&h->part, (void**)&h->scal};
   for (auto p : bufs) dfree(p);
+  dfree((void**)&h->res_rec);
+  h->res_state = 0;  // the resident plan is sized for the batch
   h->B = 0;
 }
 
@@ -1220,6 +1231,289 @@ int fold_out(sg_handle* h, void* out, int accumulate) {
   return SG_OK;
 }
 
+// ---- cluster-resident whole-sweep kernels (sg_resident.cuh) -------------------
+
+bool res_enabled(const sg_handle* h) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("SG_RESIDENT");
+    env = e ? atoi(e) : 0;
+  }
+  // opt-in: measured slower than the one-step kernels on B200 at C1/C3
+  // (cluster waves leave a third of the SMs idle, 1 CTA/SM)
+  const int want = env != 0 ? env : h->d.resident;
+  return h->esz == 4 && want > 0 && h->d.step_mode != 2;
+}
+
+template <typename T, int R>
+int res_plan_r(sg_handle* h) {
+  using K = decltype(&k_resident<T, R, true, true, false>);
+  const K probe = k_resident<T, R, true, true, false>;
+  int optin = 0;
+  SG_CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->d.device));
+  const int nzp = h->nzp, nxp = h->nxp;
+  const int runs = (nzp + kResNR - 1) / kResNR;
+  const int hrows = std::min(nzp, 256), hboxes = (nzp + 255) / 256;
+  double best = 1e300;
+  int bCL = 0, bW = 0, bthreads = 0, bclusters = 0;
+  for (int CL = 2; CL <= 16; ++CL) {
+    const int W = (((nxp + CL - 1) / CL) + 3) / 4 * 4;
+    if ((nxp + W - 1) / W != CL || W > 256 || W < 8) continue;
+    const int Q = W / 4;
+    const int threads = (Q * runs + 31) / 32 * 32;
+    if (threads > kResMaxThreads) continue;
+    const int SR = runs * kResNR + 2 * kResHW;
+    const int smem = ResSmem<T>(true, SR, W, hrows, hboxes).bytes;
+    if (smem > optin - 8192) continue;  // static shared memory (receiver staging) on top
+    if (cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+        cudaFuncSetAttribute(probe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL * 64);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, probe, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (nc < 1) continue;
+    // waves of clusters x per-step work of one CTA (cells + a barrier's worth)
+    const int shots = std::max(1, h->B);
+    const double cost = (double)((shots + nc - 1) / nc) * ((double)W * nzp + 3000.0);
+    if (cost < best) {
+      best = cost;
+      bCL = CL;
+      bW = W;
+      bthreads = threads;
+      bclusters = nc;
+    }
+  }
+  if (bCL == 0) {
+    h->res_state = -1;
+    return SG_OK;
+  }
+  h->res_CL = bCL;
+  h->res_W = bW;
+  h->res_Q = bW / 4;
+  h->res_runs = runs;
+  h->res_SW = bW;
+  h->res_SR = runs * kResNR + 2 * kResHW;
+  h->res_hrows = hrows;
+  h->res_hboxes = hboxes;
+  h->res_threads = bthreads;
+  h->res_clusters = bclusters;
+  // receivers by owner CTA (the column quad run holding the leftmost tap);
+  // tap offsets into the owner's shared plane
+  const int NRc = h->d.n_rec;
+  std::vector<int> off(4 * NRc), owner(NRc), list, start(bCL + 1, 0);
+  for (int r = 0; r < NRc; ++r) {
+    int cmin = 1 << 30;
+    for (int k = 0; k < 4; ++k) cmin = std::min(cmin, h->rec_cols_h[k * NRc + r]);
+    owner[r] = cmin / bW;
+    const int c0 = owner[r] * bW;
+    for (int k = 0; k < 4; ++k) {
+      const int rr = h->rec_rows_h[k * NRc + r], cc = h->rec_cols_h[k * NRc + r];
+      if (cc - c0 < -kResHW || cc - c0 >= bW + kResHW) {
+        h->res_state = -1;  // taps wider than the halo (not bilinear): one-step kernels
+        return SG_OK;
+      }
+      // own plane offset, or -1 - (offset into the halo slot [left | right])
+      const int hr4 = (rr + kResHW) * 4;
+      if (cc < c0) off[k * NRc + r] = -1 - (hr4 + cc - (c0 - 4));
+      else if (cc >= c0 + bW) off[k * NRc + r] = -1 - (h->res_SR * 4 + hr4 + cc - (c0 + bW));
+      else off[k * NRc + r] = (rr + kResHW) * bW + (cc - c0);
+    }
+    start[owner[r] + 1]++;
+  }
+  for (int c = 0; c < bCL; ++c) start[c + 1] += start[c];
+  list.resize(NRc);
+  {
+    std::vector<int> fill(start.begin(), start.end() - 1);
+    for (int r = 0; r < NRc; ++r) list[fill[owner[r]]++] = r;
+  }
+  std::vector<int> all(off);
+  all.insert(all.end(), list.begin(), list.end());
+  all.insert(all.end(), start.begin(), start.end());
+  dfree((void**)&h->res_rec);
+  SG_TRY(dalloc(h, (void**)&h->res_rec, all.size() * sizeof(int)));
+  SG_CK(cudaMemcpy(h->res_rec, all.data(), all.size() * sizeof(int), cudaMemcpyHostToDevice));
+  if (!h->wav_dev) SG_TRY(upload_cast<T>(h, &h->wav_dev, h->wavelet.data(), h->wavelet.size()));
+  h->res_state = 1;
+  return SG_OK;
+}
+
+// whether this handle's sweeps run as resident launches (plans on first use)
+template <typename T>
+bool res_ready(sg_handle* h) {
+  if constexpr (sizeof(T) != 4) {
+    return false;
+  } else {
+    if (!res_enabled(h)) return false;
+    if (h->res_state == 0) {
+      const int rc = h->d.order == 8 ? res_plan_r<T, 4>(h) : res_plan_r<T, 1>(h);
+      if (rc != SG_OK) {
+        cudaGetLastError();
+        h->res_state = -1;
+      }
+    }
+    if (h->res_state > 0 && !h->wav_dev &&
+        upload_cast<T>(h, &h->wav_dev, h->wavelet.data(), h->wavelet.size()) != SG_OK)
+      h->res_state = -1;
+    return h->res_state > 0;
+  }
+}
+
+template <typename T>
+void res_common(const sg_handle* h, ResArgs<T>& a, int cnt) {
+  std::memset(&a, 0, sizeof(a));
+  (void)cnt;
+  a.inv_m = field<T>(h->inv_m_buf, h);
+  a.pz = reinterpret_cast<const T*>(h->pz_buf) + kGuard;
+  a.px = reinterpret_cast<const T*>(h->px_buf) + kGuard;
+  a.nzp = h->nzp;
+  a.nxp = h->nxp;
+  a.ldx = h->ldx;
+  a.W = h->res_W;
+  a.CL = h->res_CL;
+  a.Q = h->res_Q;
+  a.runs = h->res_runs;
+  a.SR = h->res_SR;
+  a.hrows = h->res_hrows;
+  a.hboxes = h->res_hboxes;
+  a.n0 = 0;
+  a.n1 = h->d.nt;
+  a.dt2 = (T)(h->d.dt * h->d.dt);
+  for (int k = 0; k < 5; ++k) {
+    a.cz[k] = (T)h->cz[k];
+    a.cx[k] = (T)h->cx[k];
+  }
+}
+
+template <typename T, int R, bool ADJ, bool HIST, bool GATHER>
+int launch_res_f(const sg_handle* h, cudaStream_t s, const ResArgs<T>& a, int cnt) {
+  const auto kern = k_resident<T, R, ADJ, HIST, GATHER>;
+  static int attr_smem = 0;
+  const int smem = ResSmem<T>(ADJ, a.SR, a.W, a.hrows, a.hboxes).bytes;
+  if (smem > attr_smem) {
+    SG_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SG_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr_smem = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cnt * a.CL);
+  cfg.blockDim = dim3(h->res_threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = a.CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  SG_CK(cudaLaunchKernelEx(&cfg, kern, a));
+  count_launch();
+  return SG_OK;
+}
+
+// resident forward sweep over all nt steps for batch shots [s0, s0 + cnt):
+// history `hr` (base nullptr: none), gathers into h->gath if `gathers`
+template <typename T>
+int enq_res_forward(sg_handle* h, cudaStream_t s, int cnt, const HistRef& hr, bool gathers,
+                    int s0 = 0) {
+  if constexpr (sizeof(T) != 4) {
+    return fail(SG_ERR_STATE, "resident sweeps are fp32 only");
+  } else {
+  ResArgs<T> a;
+  res_common<T>(h, a, cnt);
+  a.s0 = s0;
+  a.src_rc = h->bsrc_rc;
+  a.src_w = reinterpret_cast<const T*>(h->bsrc_w);
+  a.wav = reinterpret_cast<const T*>(h->wav_dev);
+  a.hist = reinterpret_cast<T*>(hr.base);
+  a.hplane = h->hplane;
+  a.hist_steps = hr.steps;
+  a.hist_n0 = hr.n0;
+  const int NRc = h->d.n_rec;
+  a.rec_w = reinterpret_cast<const T*>(h->rec_w);
+  a.rec_off = h->res_rec;
+  a.rec_list = h->res_rec + 4 * NRc;
+  a.rec_start = h->res_rec + 5 * NRc;
+  a.nrec = NRc;
+  a.gather = gathers ? reinterpret_cast<T*>(h->gath) : nullptr;
+  a.gather_stride = (int64_t)h->d.nt * NRc;
+  const bool hi = hr.base != nullptr;
+#define RES_F(RR)                                                                         \
+  do {                                                                                    \
+    if (hi && gathers) return launch_res_f<T, RR, false, true, true>(h, s, a, cnt);       \
+    if (hi) return launch_res_f<T, RR, false, true, false>(h, s, a, cnt);                 \
+    if (gathers) return launch_res_f<T, RR, false, false, true>(h, s, a, cnt);            \
+    return launch_res_f<T, RR, false, false, false>(h, s, a, cnt);                        \
+  } while (0)
+  if (h->d.order == 8) RES_F(4);
+  RES_F(1);
+#undef RES_F
+  }
+}
+
+// resident adjoint sweep (steps nt-1 .. 0) imaging against history `hr`,
+// R^T y from the dense band array; per-shot images into h->img planes [0, B)
+template <typename T>
+int enq_res_adjoint(sg_handle* h, cudaStream_t s, int cnt, const HistRef& hr, int s0 = 0) {
+  if constexpr (sizeof(T) != 4) {
+    return fail(SG_ERR_STATE, "resident sweeps are fp32 only");
+  } else {
+  ResArgs<T> a;
+  res_common<T>(h, a, cnt);
+  a.s0 = s0;
+  a.hist_steps = hr.steps;
+  a.hist_n0 = hr.n0;
+  {
+    char keyb[96];
+    snprintf(keyb, sizeof keyb, "res/%p/%lld/%d", hr.base, (long long)(hr.shots * hr.steps),
+             h->res_W);
+    auto it = h->tmaps.find(keyb);
+    if (it == h->tmaps.end()) {
+      EncodeTiledFn enc = encode_fn();
+      if (!enc) return fail(SG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+      cuuint64_t dims[3] = {(cuuint64_t)h->ldx, (cuuint64_t)h->nzp,
+                            (cuuint64_t)(hr.shots * hr.steps)};
+      cuuint64_t strides[2] = {(cuuint64_t)h->ldx * sizeof(T), (cuuint64_t)h->hplane * sizeof(T)};
+      cuuint32_t box[3] = {(cuuint32_t)h->res_W, (cuuint32_t)h->res_hrows, 1};
+      cuuint32_t estr[3] = {1, 1, 1};
+      CUtensorMap m;
+      CUresult r = enc(&m, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                       3, hr.base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS)
+        return fail(SG_ERR_CUDA, "cuTensorMapEncodeTiled (resident history) failed: " +
+                                     std::to_string((int)r));
+      it = h->tmaps.emplace(keyb, m).first;
+    }
+    a.h_map = it->second;
+  }
+  a.inj_dense = reinterpret_cast<const T*>(h->inj_dense);
+  a.inj_stride = (int64_t)h->d.nt * h->inj_nrows * h->nxp;
+  a.inj_row0 = h->inj_row0;
+  a.inj_nrows = h->inj_nrows;
+  a.image = reinterpret_cast<T*>(h->img);
+  a.image_stride = h->hplane;
+  if (h->d.order == 8) return launch_res_f<T, 4, true, true, false>(h, s, a, cnt);
+  return launch_res_f<T, 1, true, true, false>(h, s, a, cnt);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // sweep drivers (typed)
 // ---------------------------------------------------------------------------
@@ -1231,6 +1525,18 @@ int do_forward_batch(sg_handle* h, int b0, int cnt, bool store_full_hist_ckpt_mo
   SG_TRY(load_batch_sources(h, b0, cnt));
   SG_TRY(zero_fields(h, true, false, cnt));
   const int nt = h->d.nt;
+  // cluster-resident sweep: one launch for the whole forward (gathers, and
+  // the acceleration history in FULL gradient mode)
+  if ((!store_full_hist_ckpt_mode || h->recon == SG_RECON_FULL) && res_ready<T>(h)) {
+    const bool hist = store_full_hist_ckpt_mode;
+    SG_TRY(run_graph(h, std::string(hist ? "res_fwd_full/" : "res_fwd_plain/") + std::to_string(cnt),
+                     [&](cudaStream_t s) -> int {
+                       HistRef hr;
+                       if (hist) hr = main_hist(h, 0);
+                       return enq_res_forward<T>(h, s, cnt, hr, true);
+                     }));
+    return SG_OK;
+  }
   if (!store_full_hist_ckpt_mode) {
     SG_TRY(run_graph(h, "fwd_plain/" + std::to_string(cnt), [&](cudaStream_t s) -> int {
       return fork_chains(h, s, cnt, [&](cudaStream_t cs, int s0, int c) -> int {
@@ -1283,6 +1589,15 @@ int do_adjoint_batch(sg_handle* h, int cnt, const void* cached_hist, int64_t cac
       hr.shots = cached_shots;
     }
     const void* hb = hr.base;
+    if (h->inj_dense && res_ready<T>(h)) {
+      // cluster-resident adjoint: one launch for the whole sweep
+      const std::string key = std::string(cached_hist ? "res_adj_cached/" : "res_adj_full/") +
+                              std::to_string(cnt) + "/" + std::to_string((uintptr_t)hb);
+      SG_TRY(run_graph(h, key, [&](cudaStream_t s) -> int {
+        return enq_res_adjoint<T>(h, s, cnt, hr);
+      }));
+      return SG_OK;
+    }
     std::string key = std::string(cached_hist ? "adj_cached/" : "adj_full/") +
                       std::to_string(cnt) + "/" + std::to_string((uintptr_t)hb);
     SG_TRY(run_graph(h, key, [&](cudaStream_t s) -> int {
@@ -1854,7 +2169,8 @@ int sg_destroy(sg_handle* h) {
   void** bufs[] = {(void**)&h->rec_rc, (void**)&h->tile_rec_ptr, (void**)&h->tile_rec,
                    &h->inv_m_buf, &h->pz_buf, &h->px_buf, &h->gscale_buf, (void**)&h->src_rc,
                    &h->src_w, (void**)&h->rec_ij, &h->rec_w, (void**)&h->inj_ptr,
-                   (void**)&h->inj_rec, &h->inj_w, &h->born_hist};
+                   (void**)&h->inj_rec, &h->inj_w, &h->born_hist, &h->wav_dev,
+                   (void**)&h->res_rec};
   for (auto p : bufs) dfree(p);
   if (h->cap) cudaStreamDestroy(h->cap);
   for (int c = 1; c < sg_handle::kMaxChains; ++c) {
@@ -1998,6 +2314,10 @@ int sg_set_geometry(sg_handle* h, const int32_t* src_rows, const int32_t* src_co
     SG_TRY(upload_cast<double>(h, &h->rec_w, rec_w, 4 * (size_t)R));
     SG_TRY(upload_cast<double>(h, &h->inj_w, iw.data(), iw.size()));
   }
+  h->rec_rows_h.assign(rec_rows, rec_rows + 4 * R);
+  h->rec_cols_h.assign(rec_cols, rec_cols + 4 * R);
+  dfree((void**)&h->res_rec);
+  h->res_state = 0;
   h->inj_row0 = rmin;
   h->inj_nrows = nrows;
   h->src_scale = src_scale;
@@ -2011,6 +2331,7 @@ int sg_set_wavelet(sg_handle* h, const double* amp) {
   for (int n = 0; n < h->d.nt; ++n)
     if (!std::isfinite(amp[n])) return fail(SG_ERR_ARG, "wavelet contains non-finite values");
   h->wavelet.assign(amp, amp + h->d.nt);
+  dfree(&h->wav_dev);
   h->have_wavelet = true;
   drop_graphs(h);  // amplitudes are baked into captured launches
   return SG_OK;
@@ -2171,6 +2492,20 @@ int sg_query(sg_handle* h, int32_t* batch, int32_t* recon, double* bytes) {
 }
 
 int sg_chains(sg_handle* h, int32_t count) { return h ? nchains(h, count) : 1; }
+
+int sg_resident_plan(sg_handle* h, int32_t* out) {
+  SG_TRY(check_handle(h, false));
+  if (!out) return fail(SG_ERR_ARG, "null output");
+  SG_TRY(ensure_batch(h));
+  const bool on = h->esz == 4 ? res_ready<float>(h) : res_ready<double>(h);
+  out[0] = on ? 1 : 0;
+  out[1] = on ? h->res_CL : 0;
+  out[2] = on ? h->res_W : 0;
+  out[3] = on ? h->res_threads : 0;
+  out[4] = on ? h->res_clusters : 0;
+  out[5] = on ? ResSmem<float>(true, h->res_SR, h->res_W, h->res_hrows, h->res_hboxes).bytes : 0;
+  return SG_OK;
+}
 
 int sg_time_step_kernel(sg_handle* h, int32_t which, int32_t count, int32_t reps, float* ms) {
   SG_TRY(check_handle(h));

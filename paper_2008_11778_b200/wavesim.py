@@ -131,7 +131,7 @@ class Propagator:
 
     def __init__(self, grid, geometry, wavelet, config=SimConfig(), dtype="float64",
                  device=None, recon="auto", batch=0, checkpoint_every=0, use_graphs=True,
-                 mem_budget_bytes=0.0, group=0, step_mode=0, chains=0):
+                 mem_budget_bytes=0.0, group=0, step_mode=0, chains=0, resident=0):
         torch = _torch()
         self.lib = _lib.load()
         if not torch.cuda.is_available():
@@ -162,6 +162,7 @@ class Propagator:
         d.group = int(group)
         d.step_mode = int(step_mode)
         d.chains = int(chains)
+        d.resident = int(resident)
         d.dx, d.dz, d.dt = grid.dx, grid.dz, geometry.dt
         d.cfl_safety = config.cfl_safety
         d.mem_budget_bytes = float(mem_budget_bytes)
@@ -335,6 +336,15 @@ class Propagator:
         _lib.check(self.lib.sg_query(self.h, C.byref(b), C.byref(r), C.byref(by)), "query")
         return dict(batch=b.value, recon={0: "full", 1: "checkpoint", 3: "boundary"}.get(r.value, r.value),
                     device_bytes=by.value)
+
+    def resident_plan(self):
+        """Cluster-resident sweep plan: whether the whole-sweep kernels run
+        (fp32 grids whose shot fits one cluster's shared memory) and their
+        launch shape."""
+        out = (C.c_int32 * 6)()
+        _lib.check(self.lib.sg_resident_plan(self.h, out), "resident_plan")
+        return dict(on=bool(out[0]), cluster=out[1], cols_per_cta=out[2], threads=out[3],
+                    clusters_resident=out[4], smem_bytes=out[5])
 
     def chains(self, count=None):
         """Concurrent shot chains a sweep over `count` shots runs as."""

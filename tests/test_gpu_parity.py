@@ -690,3 +690,37 @@ def test_partial_born_cache(monkeypatch):
     lv2, lg2 = p.lsrtm_gradient(m_r * 0.3, d)
     assert abs(lv2 - lv) <= 1e-12 * abs(lv)
     assert rel(lg2.cpu().numpy(), lg.cpu().numpy()) <= 1e-12
+
+
+def test_resident_sweeps_match_one_step():
+    """fp32 cluster-resident whole-sweep kernels (opt-in, desc.resident=1):
+    gathers / misfit bitwise those of the one-step kernels (same arithmetic
+    per cell), gradients and Born images to summation-order round-off (per-shot
+    instead of per-group image planes), and the fp32 gradient within the
+    north-star tolerance of the fp64 reference golden."""
+    _, wavesim = _api()
+    case = c1(8)
+    g = case["gold"]
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    st = oracle_setup(g["m_true"], grid, geom, cfg)
+    obs = np.stack(oracle.fwi_synthetic(st, wav.samples, geom.nt, threads=5))
+    out = []
+    for res in (-1, 1):
+        p = wavesim.Propagator(grid, geom, wav, cfg, dtype="float32", recon="full",
+                               resident=res)
+        p.set_model(g["m_init"])
+        plan = p.resident_plan()
+        assert plan["on"] == (res == 1)
+        syn = p.synthetic()
+        mis = p.misfit(obs)
+        v, gr = p.gradient(obs)
+        p.born_cache()
+        img = p.born_adjoint(syn)
+        out.append((syn, mis, v, gr, img))
+    (s0, m0, v0, g0, i0), (s1, m1, v1, g1, i1) = out
+    assert torch.equal(s0, s1)
+    assert m0 == m1 and v0 == v1
+    assert rel(g1.cpu().numpy(), g0.cpu().numpy()) <= 1e-6
+    assert rel(i1.cpu().numpy(), i0.cpu().numpy()) <= 1e-6
+    assert abs(v1 - float(g["value"])) <= F32 * float(g["value"])
+    assert rel(g1.cpu().numpy(), g["grad"]) <= F32
