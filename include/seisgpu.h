@@ -206,7 +206,12 @@ int64_t sg_launch_count(void);
  * with one fused pass per push; the m x m least-squares solve runs on the
  * host in fp64 and reproduces the reference's window decisions
  * (append-after-first-push, drop when ncols > memory, rank safeguard
- * min|diag R| <= 1e-12 ||R||_F, zero basis for dependent columns). */
+ * min|diag R| <= 1e-12 ||R||_F, zero basis for dependent columns).
+ * Windows the fp64 Gram cannot resolve (a Cholesky pivot with
+ * rho^2 <= 1e-10 ||a||^2) are re-factored by a device thin QR with CGS2
+ * appends in fp64 -- the reference's own append_column
+ * (seisopt/optim/qr.py:34-60) -- and solved with its Q^T f and explicit
+ * residual (qr.py:82-95). */
 int sg_aa_create(int64_t n, int32_t memory, int32_t dtype, int32_t device, sg_aa** out);
 int sg_aa_destroy(sg_aa* a);
 int sg_aa_set_stream(sg_aa* a, void* cuda_stream);
@@ -222,6 +227,11 @@ int sg_aa_step(sg_aa* a, double beta, const double* gamma_host, const double* al
                void* p_out_dev);
 /* ||f_k||_2 (anderson.py:329) */
 int sg_aa_fk_norm(sg_aa* a, double* out_host);
+/* QR policy: 0 = Gram with the device-QR fallback (default), 1 = always the
+ * device QR (SlidingQR semantics for every window). */
+int sg_aa_set_qr(sg_aa* a, int32_t mode);
+/* Whether the current window's R came from the device QR; QR passes run. */
+int sg_aa_qr_info(sg_aa* a, int32_t* active_host, int64_t* passes_host);
 
 /* Device vector helpers for the optimizer loop (anderson.py:322, :362-370):
  *  sg_vec_axpby      : z = a x + b y  (a == 1: z = x + b y, i.e. p - eta g)

@@ -91,6 +91,8 @@ SIGNATURES = {
     "sg_aa_weights": (C.c_int, [_P, _DP, _DP, _DP, _IP]),
     "sg_aa_step": (C.c_int, [_P, _D, _DP, _DP, _P]),
     "sg_aa_fk_norm": (C.c_int, [_P, _DP]),
+    "sg_aa_set_qr": (C.c_int, [_P, _I32]),
+    "sg_aa_qr_info": (C.c_int, [_P, _IP, C.POINTER(C.c_int64)]),
     "sg_vec_axpby": (C.c_int, [_I64, _I32, _D, _P, _D, _P, _P, _P]),
     "sg_vec_lerp": (C.c_int, [_I64, _I32, _P, _P, _D, _P, _P]),
     "sg_vec_blend_dots": (C.c_int, [_I64, _I32, _P, _P, _P, _P, _DP, _P]),

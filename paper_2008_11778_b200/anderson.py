@@ -89,8 +89,11 @@ class WeightSolution:
 class AAWindow:
     """Sliding AA history held on the GPU (seisopt/optim/anderson.py:55-112)."""
 
-    def __init__(self, dim, memory, dtype="float64", device=None):
+    def __init__(self, dim, memory, dtype="float64", device=None, qr="auto"):
         torch = _torch()
+        if qr not in ("auto", "always"):
+            raise ValueError("qr must be 'auto' (Gram, device QR when it cannot resolve "
+                             "the window) or 'always'")
         if memory < 0:
             raise ValueError("memory must be non-negative")
         self.dim = int(dim)
@@ -106,6 +109,8 @@ class AAWindow:
                                          self.device.index, C.byref(h)), "sg_aa_create")
         self.h = h
         self._numpy_io = False
+        if qr == "always":
+            _lib.check(self.lib.sg_aa_set_qr(h, 1), "sg_aa_set_qr")
 
     def __del__(self):
         try:
@@ -142,6 +147,12 @@ class AAWindow:
             raise ValueError(f"vectors must have {self.dim} entries")
         self._set_stream()
         _lib.check(self.lib.sg_aa_push(self.h, _lib.dptr(pd), _lib.dptr(gd)), "push")
+
+    def qr_info(self):
+        """(current window factored by the device QR?, QR passes run so far)."""
+        act, passes = C.c_int32(), C.c_int64()
+        _lib.check(self.lib.sg_aa_qr_info(self.h, C.byref(act), C.byref(passes)), "qr_info")
+        return bool(act.value), int(passes.value)
 
     def f_k_norm(self):
         out = C.c_double()

@@ -251,6 +251,64 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Device thin-QR passes (the fallback for windows the fp64 Gram cannot
+// resolve; reproduces SlidingQR.append_column's CGS2, seisopt/optim/qr.py:34-60):
+//   mode 0: x = a (cast to fp64)           -> w = x; partials <q_i, x>, <x, x>
+//   mode 1: x = w - sum_i h_i q_i          -> w = x; partials <q_i, x>, <x, x>
+//   mode 2: q_nq = h_0 > 0 ? w / h_0 : 0   (normalise into basis column nq)
+// q_i = Q + i ld (fp64).  Partials: nq + 1 per block.
+template <typename T, int MW>
+__global__ void __launch_bounds__(kThreads)
+    k_qr_pass(const T* __restrict__ a, double* __restrict__ w, double* __restrict__ Q,
+              int64_t n, int64_t ld, int nq, const Coefs h, int mode,
+              double* __restrict__ part) {
+  double acc[MW];
+#pragma unroll
+  for (int i = 0; i < MW; ++i) acc[i] = 0.0;
+  double xx = 0.0;
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = gtid; e < n; e += gstride) {
+    if (mode == 2) {
+      Q[(int64_t)nq * ld + e] = h.c[0] > 0.0 ? w[e] / h.c[0] : 0.0;
+      continue;
+    }
+    double x;
+    if (mode == 0) {
+      x = (double)a[e];
+    } else {
+      x = w[e];
+#pragma unroll
+      for (int i = 0; i < MW; ++i)
+        if (i < nq) x -= h.c[i] * Q[(int64_t)i * ld + e];
+    }
+    w[e] = x;
+#pragma unroll
+    for (int i = 0; i < MW; ++i)
+      if (i < nq) acc[i] += Q[(int64_t)i * ld + e] * x;
+    xx += x * x;
+  }
+  if (mode == 2) return;
+  const int na = nq + 1;
+  __shared__ double red[kThreads / 32][kMaxMem + 2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  auto warp_put = [&](int idx, double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[wid][idx] = v;
+  };
+#pragma unroll
+  for (int i = 0; i < MW; ++i)
+    if (i < nq) warp_put(i, acc[i]);
+  warp_put(nq, xx);
+  __syncthreads();
+  for (int k = threadIdx.x; k < na; k += blockDim.x) {
+    double sum = 0.0;
+    for (int w2 = 0; w2 < kThreads / 32; ++w2) sum += red[w2][k];
+    part[(int64_t)blockIdx.x * na + k] = sum;
+  }
+}
+
 // ---- vector helpers ------------------------------------------------------------
 
 template <typename T>
@@ -398,6 +456,14 @@ struct sg_aa {
   std::vector<double> gram;  // memory x memory, window order
   std::vector<double> bvec;  // <DF_i, f_k>
   double fk2 = 0.0;
+  // device QR fallback (windows the Gram cannot resolve, or mode 1 = always):
+  // fp64 basis Q (memory columns + one scratch column) and R of the current
+  // window, valid while qr_active
+  int qr_mode = 0;
+  double* Qd = nullptr;
+  bool qr_active = false;
+  std::vector<double> Rq;
+  int64_t qr_passes = 0;  // device QR passes run (diagnostics)
   // cached weights of the current window
   bool have_w = false;
   std::vector<double> gamma, alpha;
@@ -425,10 +491,14 @@ void drop_oldest(sg_aa* a) {
 // Cholesky R (upper, R^T R = Gram) with the reference's dependence rule: a
 // pivot is zero when rho < 1e-15 max(||a||, 1) (qr.py:47-53) or when it is
 // below the Gram formulation's resolution (rho^2 <= 1e-14 ||a||^2).
-void cholesky(const sg_aa* a, std::vector<double>& R, std::vector<double>& diag) {
+// Returns true when a pivot is below what the fp64 Gram resolves reliably
+// (rho^2 <= 1e-10 ||a||^2, i.e. rho / ||a|| <= 1e-5): the window then takes the
+// device QR instead.
+bool cholesky(const sg_aa* a, std::vector<double>& R, std::vector<double>& diag) {
   const int k = a->ncols, m = a->memory;
   R.assign((size_t)k * k, 0.0);
   diag.assign(k, 0.0);
+  bool unresolved = false;
   for (int j = 0; j < k; ++j) {
     const double ajj = a->gram[(size_t)j * m + j];
     for (int i = 0; i < j; ++i) {
@@ -440,48 +510,150 @@ void cholesky(const sg_aa* a, std::vector<double>& R, std::vector<double>& diag)
     for (int l = 0; l < j; ++l) s -= R[(size_t)l * k + j] * R[(size_t)l * k + j];
     const double nrm = std::sqrt(std::max(ajj, 0.0));
     double rho = s > 0.0 ? std::sqrt(s) : 0.0;
+    if (s <= 1e-10 * ajj) unresolved = true;
     if (rho <= 1e-300 || rho < 1e-15 * std::max(nrm, 1.0) || s <= 1e-14 * ajj) rho = 0.0;
     diag[j] = rho;
     R[(size_t)j * k + j] = rho;
   }
+  return unresolved;
+}
+
+// one k_qr_pass launch + fixed-order partial sums -> host (nq + 1 values)
+template <typename T>
+int qr_pass(sg_aa* a, const T* col, int nq, const double* h, int mode, std::vector<double>* o) {
+  const int nb = grid_for(a->n);
+  Coefs cf{};
+  for (int i = 0; i < (mode == 2 ? 1 : nq); ++i) cf.c[i] = h ? h[i] : 0.0;
+  double* w = a->Qd + (int64_t)a->memory * a->ld;  // scratch column
+  const int mw = std::max(nq, 1);
+#define QRP(MW) k_qr_pass<T, MW><<<nb, kThreads, 0, a->stream>>>(col, w, a->Qd, a->n, a->ld, nq, cf, mode, a->part)
+  if (mw <= 4) QRP(4);
+  else if (mw <= 8) QRP(8);
+  else if (mw <= 16) QRP(16);
+  else QRP(32);
+#undef QRP
+  count_launch();
+  a->qr_passes++;
+  if (mode == 2) return SG_OK;
+  const int na = nq + 1;
+  k_sum_cols<<<na, 256, 0, a->stream>>>(a->part, nb, na, a->out);
+  count_launch();
+  SG_CK(cudaGetLastError());
+  o->resize(na);
+  SG_CK(cudaMemcpyAsync(o->data(), a->out, na * sizeof(double), cudaMemcpyDeviceToHost, a->stream));
+  SG_CK(cudaStreamSynchronize(a->stream));
+  return SG_OK;
+}
+
+// Thin QR of the current window (oldest column first) by CGS2 appends, the
+// reference's append_column (seisopt/optim/qr.py:34-60): h = Q^T a,
+// w = a - Q h, h2 = Q^T w, w -= Q h2, rho = ||w|| (zero basis when
+// rho < 1e-15 max(||a||, 1)).  R (k x k, row-major) into a->Rq.
+template <typename T>
+int device_qr(sg_aa* a) {
+  const int k = a->ncols;
+  if (!a->Qd) {
+    const size_t bytes = (size_t)(a->memory + 1) * a->ld * sizeof(double);
+    cudaError_t e = cudaMalloc((void**)&a->Qd, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      a->Qd = nullptr;
+      return fail(SG_ERR_OOM, std::string("AA QR basis allocation failed: ") + cudaGetErrorString(e));
+    }
+  }
+  a->Rq.assign((size_t)k * k, 0.0);
+  const T* DF = reinterpret_cast<const T*>(a->DF);
+  std::vector<double> o0, o1, o2;
+  for (int j = 0; j < k; ++j) {
+    const T* col = DF + (int64_t)slot_of(a, j) * a->ld;
+    SG_TRY(qr_pass<T>(a, col, j, nullptr, 0, &o0));            // h = Q^T a, ||a||^2
+    SG_TRY(qr_pass<T>(a, (const T*)nullptr, j, o0.data(), 1, &o1));  // w = a - Q h; h2
+    SG_TRY(qr_pass<T>(a, (const T*)nullptr, j, o1.data(), 1, &o2));  // w -= Q h2; ||w||^2
+    for (int i = 0; i < j; ++i) a->Rq[(size_t)i * k + j] = o0[i] + o1[i];
+    double rho = std::sqrt(std::max(o2[j], 0.0));
+    const double scale = std::max(std::sqrt(std::max(o0[j], 0.0)), 1.0);
+    if (rho <= 1e-300 || rho < 1e-15 * scale) rho = 0.0;
+    a->Rq[(size_t)j * k + j] = rho;
+    SG_TRY(qr_pass<T>(a, (const T*)nullptr, j, &rho, 2, nullptr));  // q_j = w / rho
+  }
+  a->qr_active = true;
+  return SG_OK;
+}
+
+// R of the current window: Cholesky of the Gram, or the device QR when the
+// Gram cannot resolve it (or qr_mode == 1)
+int window_r(sg_aa* a, std::vector<double>& R, std::vector<double>& d) {
+  const bool unresolved = cholesky(a, R, d);
+  a->qr_active = false;
+  if (!unresolved && a->qr_mode != 1) return SG_OK;
+  SG_TRY(a->esz == 4 ? device_qr<float>(a) : device_qr<double>(a));
+  R = a->Rq;
+  const int k = a->ncols;
+  for (int j = 0; j < k; ++j) d[j] = std::fabs(R[(size_t)j * k + j]);
+  return SG_OK;
 }
 
 // safeguard (anderson.py:105-112): shed oldest columns while
 // min|diag R| <= 1e-12 ||R||_F
-void safeguard(sg_aa* a) {
+int safeguard(sg_aa* a) {
   std::vector<double> R, d;
   while (a->ncols > 0) {
-    cholesky(a, R, d);
+    SG_TRY(window_r(a, R, d));
     double fro2 = 0.0;
     for (double v : R) fro2 += v * v;
     const double tol = 1e-12 * std::max(std::sqrt(fro2), 1e-300);
     if (*std::min_element(d.begin(), d.end()) > tol) break;
     drop_oldest(a);
+    a->qr_active = false;
   }
+  return SG_OK;
+}
+
+// gamma = solve_triangular(R, Q^T f) and ||f - Q Q^T f|| with the device basis
+// (seisopt/optim/qr.py:82-95)
+template <typename T>
+int qr_solve(sg_aa* a, std::vector<double>& gmm, double& resid) {
+  const int k = a->ncols;
+  std::vector<double> qf, rr;
+  SG_TRY(qr_pass<T>(a, reinterpret_cast<const T*>(a->fk), k, nullptr, 0, &qf));  // Q^T f, ||f||^2
+  SG_TRY(qr_pass<T>(a, (const T*)nullptr, k, qf.data(), 1, &rr));               // ||f - Q Q^T f||^2
+  gmm.assign(k, 0.0);
+  const std::vector<double>& R = a->Rq;
+  for (int i = k - 1; i >= 0; --i) {
+    double s = qf[i];
+    for (int l = i + 1; l < k; ++l) s -= R[(size_t)i * k + l] * gmm[l];
+    gmm[i] = s / R[(size_t)i * k + i];
+  }
+  resid = std::min(std::sqrt(std::max(rr[k], 0.0)), std::sqrt(std::max(qf[k], 0.0)));
+  return SG_OK;
 }
 
 int compute_weights(sg_aa* a) {
   const int k = a->ncols;
   if (k == 0 || a->pushes < 2) return fail(SG_ERR_EMPTY, "aa_weights needs at least one stored difference");
-  std::vector<double> R, d;
-  cholesky(a, R, d);
-  // forward solve R^T y = b, back solve R gamma = y  (== solve_triangular(R, Q^T f))
-  std::vector<double> y(k), gmm(k);
-  for (int i = 0; i < k; ++i) {
-    double s = a->bvec[i];
-    for (int l = 0; l < i; ++l) s -= R[(size_t)l * k + i] * y[l];
-    y[i] = s / R[(size_t)i * k + i];
+  std::vector<double> R, d, gmm(k);
+  if (!a->qr_active) SG_TRY(window_r(a, R, d));
+  if (a->qr_active) {
+    SG_TRY(a->esz == 4 ? qr_solve<float>(a, gmm, a->resid) : qr_solve<double>(a, gmm, a->resid));
+  } else {
+    // forward solve R^T y = b, back solve R gamma = y  (== solve_triangular(R, Q^T f))
+    std::vector<double> y(k);
+    for (int i = 0; i < k; ++i) {
+      double s = a->bvec[i];
+      for (int l = 0; l < i; ++l) s -= R[(size_t)l * k + i] * y[l];
+      y[i] = s / R[(size_t)i * k + i];
+    }
+    for (int i = k - 1; i >= 0; --i) {
+      double s = y[i];
+      for (int l = i + 1; l < k; ++l) s -= R[(size_t)i * k + l] * gmm[l];
+      gmm[i] = s / R[(size_t)i * k + i];
+    }
+    // residual ||f - A gamma||^2 = ||f||^2 - ||y||^2, clipped to [0, ||f||^2]
+    double y2 = 0.0;
+    for (double v : y) y2 += v * v;
+    const double r2 = std::max(a->fk2 - y2, 0.0);
+    a->resid = std::min(std::sqrt(r2), std::sqrt(a->fk2));
   }
-  for (int i = k - 1; i >= 0; --i) {
-    double s = y[i];
-    for (int l = i + 1; l < k; ++l) s -= R[(size_t)i * k + l] * gmm[l];
-    gmm[i] = s / R[(size_t)i * k + i];
-  }
-  // residual ||f - A gamma||^2 = ||f||^2 - ||y||^2, clipped to [0, ||f||^2]
-  double y2 = 0.0;
-  for (double v : y) y2 += v * v;
-  const double r2 = std::max(a->fk2 - y2, 0.0);
-  a->resid = std::min(std::sqrt(r2), std::sqrt(a->fk2));
   // alpha recovery with fsum fix-up (anderson.py:41-52)
   std::vector<double> al(k + 1);
   al[0] = gmm[0];
@@ -509,6 +681,7 @@ int push_t(sg_aa* a, const void* p, const void* g) {
   if (!first) {
     // a full window drops its oldest column now; the new difference takes its slot
     if (a->ncols == a->memory) drop_oldest(a);
+    a->qr_active = false;
     nw = a->ncols;
     for (int i = 0; i < nw; ++i) sl.s[i] = slot_of(a, i);
     snew = slot_of(a, nw);
@@ -568,8 +741,8 @@ int push_t(sg_aa* a, const void* p, const void* g) {
   a->ncols = nw + 1;
   a->pushes += 1;
   (void)m;
-  safeguard(a);
-  return SG_OK;
+  a->qr_active = false;
+  return safeguard(a);
 }
 
 template <typename T>
@@ -649,7 +822,7 @@ int sg_aa_create(int64_t n, int32_t memory, int32_t dtype, int32_t device, sg_aa
 int sg_aa_destroy(sg_aa* a) {
   if (!a) return SG_OK;
   cudaSetDevice(a->device);
-  for (void* p : {a->DF, a->DG, a->fk, a->gk, (void*)a->part, (void*)a->out})
+  for (void* p : {a->DF, a->DG, a->fk, a->gk, (void*)a->part, (void*)a->out, (void*)a->Qd})
     if (p) cudaFree(p);
   delete a;
   return SG_OK;
@@ -666,6 +839,7 @@ int sg_aa_clear(sg_aa* a) {
   a->head = a->ncols = a->pushes = 0;
   std::fill(a->gram.begin(), a->gram.end(), 0.0);
   a->have_w = false;
+  a->qr_active = false;
   return SG_OK;
 }
 
@@ -673,6 +847,22 @@ int sg_aa_push(sg_aa* a, const void* p, const void* g) {
   if (!a || !p || !g) return fail(SG_ERR_ARG, "null argument");
   SG_CK(cudaSetDevice(a->device));
   return a->esz == 4 ? push_t<float>(a, p, g) : push_t<double>(a, p, g);
+}
+
+int sg_aa_set_qr(sg_aa* a, int32_t mode) {
+  if (!a) return fail(SG_ERR_ARG, "null window");
+  if (mode != 0 && mode != 1) return fail(SG_ERR_ARG, "qr mode must be 0 (auto) or 1 (always)");
+  a->qr_mode = mode;
+  a->qr_active = false;
+  a->have_w = false;
+  return SG_OK;
+}
+
+int sg_aa_qr_info(sg_aa* a, int32_t* active, int64_t* passes) {
+  if (!a) return fail(SG_ERR_ARG, "null window");
+  if (active) *active = a->qr_active ? 1 : 0;
+  if (passes) *passes = a->qr_passes;
+  return SG_OK;
 }
 
 int sg_aa_m_k(sg_aa* a) {

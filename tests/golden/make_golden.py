@@ -219,6 +219,46 @@ def make_aa_window():
         step_half=np.stack([r["step_half"] for r in recs]), **versions())
 
 
+def make_aa_illcond():
+    """Window sequence with nearly dependent residual differences
+    (rho / ||a|| = 1e-6 .. 1e-9: below what a Gram / Cholesky solve resolves,
+    above the 1e-12 rank safeguard) and one the safeguard sheds (1e-14)."""
+    use_order(2)
+    rng = np.random.default_rng(23)
+    n, memory = 400, 5
+    win = A.AAWindow(n, memory)
+    ps, gs, recs = [], [], []
+    eps = {4: 1e-6, 6: 1e-8, 8: 1e-9, 10: 1e-14, 12: 1e-7}
+    for k in range(14):
+        p = rng.standard_normal(n)
+        g = rng.standard_normal(n)
+        if k in eps and k >= 2:
+            f1 = gs[k - 1] - ps[k - 1]
+            f2 = gs[k - 2] - ps[k - 2]
+            d = f1 - f2
+            noise = rng.standard_normal(n)
+            noise *= eps[k] * np.linalg.norm(d) / np.linalg.norm(noise)
+            g = p + f1 + 0.7 * d + noise  # f_k - f_{k-1} = 0.7 (f_{k-1} - f_{k-2}) + noise
+        ps.append(p)
+        gs.append(g)
+        win.push(p, g)
+        rec = dict(m_k=win.m_k)
+        w = A.aa_weights(win) if win.m_k > 0 else None
+        gamma = np.zeros(memory)
+        if w is not None:
+            gamma[: len(w.gamma)] = w.gamma
+        rec.update(gamma=gamma, resid=w.residual_norm if w is not None else np.nan,
+                   step1=A.aa_step(win, 1.0, w) if w is not None else A.aa_step(win),
+                   diag=np.pad(win.qr.diag(), (0, memory - win.qr.ncols)))
+        recs.append(rec)
+    np.savez_compressed(
+        os.path.join(HERE, "aa_illcond.npz"), n=n, memory=memory, ps=np.stack(ps),
+        gs=np.stack(gs), m_k=np.array([r["m_k"] for r in recs]),
+        gamma=np.stack([r["gamma"] for r in recs]), resid=np.array([r["resid"] for r in recs]),
+        step1=np.stack([r["step1"] for r in recs]), diag=np.stack([r["diag"] for r in recs]),
+        **versions())
+
+
 def make_aa_run():
     """aa_run on a contractive affine fixed point G(p) = M p + c (beta 1 and
     0.7), and Armijo steepest descent on the small FWI problem."""
@@ -264,6 +304,7 @@ if __name__ == "__main__":
             globals()[name]()
         sys.exit(0)
     make_aa_window()
+    make_aa_illcond()
     make_aa_run()
     for order in (2, 8):
         for top in (True, False):

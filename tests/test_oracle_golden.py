@@ -82,6 +82,24 @@ def test_aa_window_sequence():
     assert int(g["m_k"][7]) < min(7, memory)
 
 
+
+def test_aa_illcond_sequence():
+    """Oracle QR window vs the reference on nearly dependent differences
+    (tests/golden/make_golden.py:make_aa_illcond): same window sizes, R
+    diagonals and weights to the conditioning of the window."""
+    g = golden("aa_illcond")
+    n, memory = int(g["n"]), int(g["memory"])
+    win = oracle.AAWindowOracle(n, memory)
+    for k in range(len(g["ps"])):
+        win.push(g["ps"][k], g["gs"][k])
+        assert win.m_k == int(g["m_k"][k]), k
+        if win.m_k:
+            w = oracle.aa_weights(win)
+            assert rel(w[0], g["gamma"][k][: win.m_k]) <= 1e-9
+            assert rel(oracle.aa_step(win, 1.0, w), g["step1"][k]) <= 1e-9
+    # the 1e-14-dependent difference pushed at k=10 triggered the safeguard
+    assert int(g["m_k"][10]) == 1
+
 def test_aa_fwi_trajectory():
     g = golden("aa_fwi_small")
     case = small_case(8, True)
