@@ -844,6 +844,7 @@ int sg_aa_clear(sg_aa* a) {
 }
 
 int sg_aa_push(sg_aa* a, const void* p, const void* g) {
+  sg::Trace trace_("sg_aa_push");
   if (!a || !p || !g) return fail(SG_ERR_ARG, "null argument");
   SG_CK(cudaSetDevice(a->device));
   return a->esz == 4 ? push_t<float>(a, p, g) : push_t<double>(a, p, g);
@@ -871,6 +872,7 @@ int sg_aa_m_k(sg_aa* a) {
 }
 
 int sg_aa_weights(sg_aa* a, double* gamma, double* alpha, double* resid, int32_t* m_k) {
+  sg::Trace trace_("sg_aa_weights");
   if (!a) return fail(SG_ERR_ARG, "null window");
   if (sg_aa_m_k(a) == 0) return fail(SG_ERR_EMPTY, "aa_weights needs at least one stored difference");
   if (!a->have_w) SG_TRY(compute_weights(a));
@@ -883,6 +885,7 @@ int sg_aa_weights(sg_aa* a, double* gamma, double* alpha, double* resid, int32_t
 }
 
 int sg_aa_step(sg_aa* a, double beta, const double* gamma, const double* alpha, void* out) {
+  sg::Trace trace_("sg_aa_step");
   (void)alpha;
   if (!a || !out) return fail(SG_ERR_ARG, "null argument");
   if (a->pushes == 0) return fail(SG_ERR_EMPTY, "aa_step on an empty window");

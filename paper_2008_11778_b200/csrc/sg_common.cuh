@@ -6,6 +6,8 @@
 #include <atomic>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "seisgpu.h"
 
 namespace sg {
@@ -30,6 +32,15 @@ inline int fail(int code, const std::string& msg) {
     int rc_ = (x);           \
     if (rc_ != SG_OK) return rc_; \
   } while (0)
+
+// NVTX range around a C-ABI call (header-only NVTX v3: a no-op unless a
+// tool such as ncu --nvtx injects itself)
+struct Trace {
+  explicit Trace(const char* name) { nvtxRangePushA(name); }
+  ~Trace() { nvtxRangePop(); }
+  Trace(const Trace&) = delete;
+  Trace& operator=(const Trace&) = delete;
+};
 
 inline void count_launch(int64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 

@@ -1720,13 +1720,19 @@ int fwi_gradient_t(sg_handle* h, int shot0, int count, const void* obs, double* 
   for (int b0 = shot0; b0 < shot0 + count; b0 += h->B) {
     const int cnt = std::min(h->B, shot0 + count - b0);
     if (timing) cudaEventRecord(ev[0], h->stream);
-    SG_TRY(do_forward_batch<T>(h, b0, cnt, true));
+    {
+      Trace t_("forward sweep");
+      SG_TRY(do_forward_batch<T>(h, b0, cnt, true));
+    }
     if (timing) cudaEventRecord(ev[1], h->stream);
     SG_TRY(residual<T>(h, cnt, reinterpret_cast<const T*>((const char*)obs + (b0 - shot0) * per),
                        0));
     SG_TRY(fill_injection<T>(h, cnt));
     if (timing) cudaEventRecord(ev[2], h->stream);
-    SG_TRY(do_adjoint_batch<T>(h, cnt, nullptr, 0));
+    {
+      Trace t_("adjoint sweep + imaging");
+      SG_TRY(do_adjoint_batch<T>(h, cnt, nullptr, 0));
+    }
     if (timing) cudaEventRecord(ev[3], h->stream);
     SG_TRY(reduce_images<T>(h, cnt));
     if (timing) {
@@ -2338,6 +2344,7 @@ int sg_set_wavelet(sg_handle* h, const double* amp) {
 }
 
 int sg_set_model(sg_handle* h, const void* m, int32_t mdt) {
+  sg::Trace trace_("sg_set_model");
   if (!h || !m) return fail(SG_ERR_ARG, "null argument");
   if (mdt != SG_F32 && mdt != SG_F64) return fail(SG_ERR_ARG, "m dtype must be 4 or 8");
   SG_CK(cudaSetDevice(h->d.device));
@@ -2404,6 +2411,7 @@ int sg_set_model(sg_handle* h, const void* m, int32_t mdt) {
 }
 
 int sg_fwi_synthetic(sg_handle* h, int32_t shot0, int32_t count, void* out) {
+  sg::Trace trace_("sg_fwi_synthetic");
   SG_TRY(check_handle(h));
   SG_TRY(check_range(h, shot0, count));
   if (!out) return fail(SG_ERR_ARG, "null output");
@@ -2411,6 +2419,7 @@ int sg_fwi_synthetic(sg_handle* h, int32_t shot0, int32_t count, void* out) {
 }
 
 int sg_fwi_misfit(sg_handle* h, int32_t shot0, int32_t count, const void* obs, double* misfit) {
+  sg::Trace trace_("sg_fwi_misfit");
   SG_TRY(check_handle(h));
   SG_TRY(check_range(h, shot0, count));
   if (!obs || !misfit) return fail(SG_ERR_ARG, "null argument");
@@ -2419,6 +2428,7 @@ int sg_fwi_misfit(sg_handle* h, int32_t shot0, int32_t count, const void* obs, d
 
 int sg_fwi_gradient(sg_handle* h, int32_t shot0, int32_t count, const void* obs, double* misfit,
                     void* grad, int32_t accumulate) {
+  sg::Trace trace_("sg_fwi_gradient");
   SG_TRY(check_handle(h));
   SG_TRY(check_range(h, shot0, count));
   if (!obs || !grad) return fail(SG_ERR_ARG, "null argument");
@@ -2426,6 +2436,7 @@ int sg_fwi_gradient(sg_handle* h, int32_t shot0, int32_t count, const void* obs,
 }
 
 int sg_born_cache(sg_handle* h, int32_t shot0, int32_t count, int32_t enable) {
+  sg::Trace trace_("sg_born_cache");
   SG_TRY(check_handle(h));
   if (!enable) {
     dfree(&h->born_hist);
@@ -2439,6 +2450,7 @@ int sg_born_cache(sg_handle* h, int32_t shot0, int32_t count, int32_t enable) {
 }
 
 int sg_born_forward(sg_handle* h, int32_t shot0, int32_t count, const void* m_r, void* out) {
+  sg::Trace trace_("sg_born_forward");
   SG_TRY(check_handle(h));
   SG_TRY(check_range(h, shot0, count));
   if (!m_r || !out) return fail(SG_ERR_ARG, "null argument");
@@ -2447,6 +2459,7 @@ int sg_born_forward(sg_handle* h, int32_t shot0, int32_t count, const void* m_r,
 
 int sg_born_adjoint(sg_handle* h, int32_t shot0, int32_t count, const void* data, void* image,
                     int32_t accumulate) {
+  sg::Trace trace_("sg_born_adjoint");
   SG_TRY(check_handle(h));
   SG_TRY(check_range(h, shot0, count));
   if (!data || !image) return fail(SG_ERR_ARG, "null argument");
@@ -2456,6 +2469,7 @@ int sg_born_adjoint(sg_handle* h, int32_t shot0, int32_t count, const void* data
 
 int sg_lsrtm_gradient(sg_handle* h, int32_t shot0, int32_t count, const void* m_r,
                       const void* d_r, double* value, void* grad, int32_t accumulate) {
+  sg::Trace trace_("sg_lsrtm_gradient");
   SG_TRY(check_handle(h));
   SG_TRY(check_range(h, shot0, count));
   if (!m_r || !d_r || !grad) return fail(SG_ERR_ARG, "null argument");
@@ -2464,6 +2478,7 @@ int sg_lsrtm_gradient(sg_handle* h, int32_t shot0, int32_t count, const void* m_
 }
 
 int sg_forward_history(sg_handle* h, int32_t shot, void* gather, void* accel) {
+  sg::Trace trace_("sg_forward_history");
   SG_TRY(check_handle(h));
   SG_TRY(check_range(h, shot, 1));
   if (!gather || !accel) return fail(SG_ERR_ARG, "null argument");
@@ -2471,6 +2486,7 @@ int sg_forward_history(sg_handle* h, int32_t shot, void* gather, void* accel) {
 }
 
 int sg_adjoint_history(sg_handle* h, const void* ybar, void* v) {
+  sg::Trace trace_("sg_adjoint_history");
   SG_TRY(check_handle(h));
   if (!ybar || !v) return fail(SG_ERR_ARG, "null argument");
   return SG_DISPATCH(h, adjoint_history_t, h, ybar, v);
