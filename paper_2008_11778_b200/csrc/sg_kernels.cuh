@@ -63,6 +63,9 @@ constexpr int kHalo = 4;
 #ifndef SG_ADJ_MINB
 #define SG_ADJ_MINB 2
 #endif
+#ifndef SG_EARLY_TMA
+#define SG_EARLY_TMA 1
+#endif
 
 template <typename T>
 struct StepArgs {
@@ -488,6 +491,16 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
       tma_load_3d(st + 2 * SM::HALO + SM::TILE, &a.r_stile, &bar[s], j0, kGuard + i0, b);
     }
   };
+#if SG_EARLY_TMA
+  // The first TMA stages only wait for the previous step's grid; issue them
+  // before the per-cell model loads below so the two latencies overlap
+  // (a CTA that starts after the previous grid finished would otherwise pay
+  // the L2 round trip of the model loads, then that of the tiles).
+  if (tid == 0) {
+    pdl_wait();
+    for (int k = 0; k < NS - 1 && k < nb; ++k) issue(k);
+  }
+#endif
   // this thread: columns (j, j + 1), rows ib .. ib + kNY - 1; every update is
   // done on the column pair with packed f32x2 arithmetic
   const int j = j0 + 2 * threadIdx.x;
@@ -530,10 +543,13 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
   }
   const P dt2p = P::make(a.dt2, a.dt2);
   // everything below reads or writes fields/states of the previous step
+  // (thread 0 already waited and put the first stages in flight, SG_EARLY_TMA)
   pdl_wait();
   pdl_launch_dependents();
+#if !SG_EARLY_TMA
   if (tid == 0)
     for (int k = 0; k < NS - 1 && k < nb; ++k) issue(k);
+#endif
 
   for (int k = 0; k < nb; ++k) {
     const int b = b0 + k;
