@@ -38,11 +38,18 @@ namespace sg {
 
 constexpr int kGuard = 4;         // zero guard rows above/below each plane
 constexpr int kTileRowsMax = 64;  // tail padding covers tiles up to this height
-// 64 x (8 kNY) tile, 256 threads = 32 column pairs x 8 row groups of kNY rows
+// 64 x (kTY kNY) tile, 32 kTY threads = 32 column pairs x kTY row groups of kNY
+// rows.  Default 64 x 16 with 128-thread CTAs (6 forward / 4 adjoint per SM):
+// measured faster than 64 x 32 with 256 threads (C3 gradient 121.1 vs 123.4 ms,
+// C5 fused reverse+adjoint step 212 vs 223 us) -- smaller CTAs start and
+// retire out of phase, so their prologue / TMA latencies overlap
 #ifndef SG_NY
 #define SG_NY 4
 #endif
-constexpr int kBX = 64, kTX = 32, kTY = 8, kNY = SG_NY, kTH = kTY * kNY;
+#ifndef SG_TY
+#define SG_TY 4
+#endif
+constexpr int kBX = 64, kTX = 32, kTY = SG_TY, kNY = SG_NY, kTH = kTY * kNY;
 constexpr int kTH2 = 32;  // tile height of the two-step kernel (sg_kernels2.cuh)
 constexpr int kThreads = kTX * kTY;
 // TMA halo boxes are always kHalo wide (the 8th-order radius); the 2nd-order
@@ -388,8 +395,9 @@ __host__ __device__ constexpr bool step_dual() {
 template <typename T, bool ADJ, int FL>
 __host__ __device__ constexpr int step_min_blocks() {
   // (fp64 dual stages are 154 KB: one CTA per SM)
-  return sizeof(T) != 4 ? (step_dual<ADJ, FL>() ? 1 : 2)
-                        : (step_dual<ADJ, FL>() ? 2 : (ADJ ? SG_ADJ_MINB : SG_FP32_MINB));
+  // (counts for 256-thread CTAs; SG_TY < 8 builds smaller CTAs, more per SM)
+  return (8 / kTY) * (sizeof(T) != 4 ? (step_dual<ADJ, FL>() ? 1 : 2)
+                                     : (step_dual<ADJ, FL>() ? 2 : (ADJ ? SG_ADJ_MINB : SG_FP32_MINB)));
 }
 
 // R^T y of one cell by a walk over its CSR taps (receiver bands too wide for
