@@ -972,7 +972,7 @@ int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, con
       a.cur = cur;
       a.ybar = yb;
       // image accumulator set of this launch's parity (PDL-safe, see k_step)
-      if (img_on) a.image = reinterpret_cast<T*>(h->img) + (int64_t)cur * h->B * h->hplane;
+      if (img_on) a.image = reinterpret_cast<T*>(h->img) + (int64_t)(SG_IMG_PARITY ? cur : 0) * h->B * h->hplane;
       if (p.band_recon) {
         a.rcur = rcur;
         a.amp = (T)h->wavelet[n];
