@@ -1,0 +1,121 @@
+"""GPU parity on the BASELINE grids (C3, C4, C5) against the CPU oracle, at
+the reduced shot counts / time-step counts the fp64 oracle finishes in
+seconds ("C4/C5: only reduced-shot / reduced-nt parity is
+feasible on the CPU oracle").
+
+Tolerances (BASELINE.json north_star): fp64 relative L2 <= 1e-10; fp32
+relative L2 <= 1e-4 per gradient.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from cases import oracle_setup, rel
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+F64 = 1e-10
+F32 = 1e-4
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _one_shot(which, shot, nt):
+    """A layered-fault case reduced to one shot of the full acquisition and
+    the first `nt` steps."""
+    from paper_2008_11778_b200 import synthetic
+    from paper_2008_11778_b200.model import AcquisitionGeometry
+    case = synthetic.layered_case(which, nt=nt)
+    g0 = case["geometry"]
+    case["geometry"] = AcquisitionGeometry((g0.sources[shot],), g0.receivers, g0.dt, g0.nt)
+    return case
+
+
+_C4 = {}
+
+
+def _c4_oracle():
+    """C4 grid (201x601 @15 m, 8th order, dt 0.5 ms, 15 Hz), shot 17 of 60,
+    first 1500 steps: the reference Born operator's data for the true
+    reflectivity and its LSRTM value/gradient at half of it (fp64)."""
+    if not _C4:
+        case = _one_shot("c4", 17, 1500)
+        grid, geom, cfg, wav = case["grid"], case["geometry"], case["config"], case["wavelet"]
+        st = oracle_setup(case["background"].m, grid, geom, cfg)
+        kern = oracle.BornOracle(st, wav.samples, geom.nt)
+        dm = case["reflectivity"].m_r
+        d_r = kern.forward(dm)
+        val, grad = oracle.lsrtm_objective(kern, 0.5 * dm, d_r)
+        _C4.update(case=case, dm=dm, d_r=np.stack(d_r), val=val, grad=grad)
+    return _C4
+
+
+@pytest.mark.parametrize("dtype,cached", [("float64", False), ("float64", True),
+                                          ("float32", False), ("float32", True)])
+def test_c4_grid_lsrtm_vs_oracle(dtype, cached):
+    """LSRTM on the C4 grid: Born data and the LSRTM gradient vs the oracle,
+    with the background recomputed in lock-step and with it cached in HBM."""
+    from paper_2008_11778_b200 import wavesim
+    c = _c4_oracle()
+    case = c["case"]
+    tol = F64 if dtype == "float64" else F32
+    p = wavesim.Propagator(case["grid"], case["geometry"], case["wavelet"], case["config"],
+                           dtype=dtype)
+    p.set_model(case["background"].m)
+    if cached:
+        p.born_cache()
+        assert p.born_cached() == (0, 1)
+    d = p.born_forward(c["dm"]).double().cpu().numpy()
+    assert rel(d, c["d_r"]) <= tol
+    v, g = p.lsrtm_gradient(0.5 * c["dm"], c["d_r"])
+    assert abs(v - c["val"]) <= tol * abs(c["val"])
+    assert rel(g.double().cpu().numpy(), c["grad"]) <= tol
+
+
+_C5 = {}
+
+
+def _c5_oracle():
+    """C5 grid (1001x3001 @3 m, 1041x3041 padded, 8th order, dt 0.25 ms,
+    20 Hz), the centre shot, first 160 steps, zero observed data (the
+    residual is the synthetic itself -- the water layer makes true and
+    initial models identical near the surface this early): fp64 oracle
+    gathers, misfit and gradient."""
+    if not _C5:
+        case = _one_shot("c5", 120, 160)
+        grid, geom, cfg, wav = case["grid"], case["geometry"], case["config"], case["wavelet"]
+        st = oracle_setup(case["init"].m, grid, geom, cfg)
+        obs = [np.zeros((geom.nt, geom.n_receivers))]
+        syn = oracle.fwi_synthetic(st, wav.samples, geom.nt)
+        val, grad, _ = oracle.fwi_gradient(st, obs, wav.samples, geom.nt)
+        _C5.update(case=case, obs=np.stack(obs), syn=np.stack(syn), val=val, grad=grad)
+    return _C5
+
+
+@pytest.mark.parametrize("dtype,recon", [("float64", "full"), ("float64", "boundary"),
+                                         ("float32", "checkpoint"),
+                                         ("float32", "boundary")])
+def test_c5_grid_gradient_vs_oracle(dtype, recon):
+    """C5 grid (the HBM-bound production size): gathers, misfit and
+    gradient vs the fp64 oracle in every reconstruction mode."""
+    from paper_2008_11778_b200 import wavesim
+    c = _c5_oracle()
+    case = c["case"]
+    assert float(np.linalg.norm(c["grad"])) > 0
+    tol = F64 if dtype == "float64" else F32
+    p = wavesim.Propagator(case["grid"], case["geometry"], case["wavelet"], case["config"],
+                           dtype=dtype, recon=recon, checkpoint_every=40)
+    p.set_model(case["init"].m)
+    syn = p.synthetic().double().cpu().numpy()
+    assert rel(syn, c["syn"]) <= tol
+    v, g = p.gradient(c["obs"])
+    assert p.query()["recon"] == recon
+    assert abs(v - c["val"]) <= tol * abs(c["val"])
+    assert rel(g.double().cpu().numpy(), c["grad"]) <= tol
+    p.close()

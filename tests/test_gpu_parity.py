@@ -512,6 +512,23 @@ def test_c3_single_shot_fp32_gradient(recon):
     assert rel(g.cpu().numpy(), grad) <= F32
 
 
+@pytest.mark.parametrize("recon", ["full", "boundary"])
+def test_c3_single_shot_fp64_gradient(recon):
+    """C3 grid, one shot, fp64 mode: misfit and gradient within 1e-10 of the
+    oracle ("fp64 <= 1e-10: ... C3 one shot"), with the stored
+    history and with boundary-saving reconstruction (4000 reverse steps)."""
+    from paper_2008_11778_b200 import wavesim
+    c = _c3_one_shot()
+    case, geom, obs, val, grad = c["case"], c["geom"], c["obs"], c["val"], c["grad"]
+    grid, cfg, wav = case["grid"], case["config"], case["wavelet"]
+    prop = wavesim.Propagator(grid, geom, wav, cfg, dtype="float64", recon=recon)
+    prop.set_model(case["init"].m)
+    v, g = prop.gradient(np.stack(obs))
+    assert prop.query()["recon"] == recon
+    assert abs(v - val) <= F64 * val
+    assert rel(g.cpu().numpy(), grad) <= F64
+
+
 def test_c1_fp32_aa_misfit_curve():
     """fp32 production path: the misfit-vs-iteration curve of 20 AA
     iterations (m=5) stays within 1% of the reference's fp64 run."""
