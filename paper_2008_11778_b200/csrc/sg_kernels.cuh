@@ -70,6 +70,9 @@ constexpr int kHalo = 4;
 #ifndef SG_ADJ_MINB
 #define SG_ADJ_MINB 2
 #endif
+#ifndef SG_ADJ3
+#define SG_ADJ3 1  // three-level one-step adjoint (FL_ADJ3); 0 = V/w increment form
+#endif
 #ifndef SG_EARLY_TMA
 #define SG_EARLY_TMA 1
 #endif
@@ -91,6 +94,7 @@ struct StepArgs {
   T* f[2];                // field buffers (row 0, col 0, shot 0)
   T* state;               // inc (forward) / w (adjoint), updated in place
   int cur;                // read f[cur], write f[cur ^ 1]
+  int adj3;               // host: dispatch the FL_ADJ3 adjoint (s_tile = f_tile[cur ^ 1])
   const T* inv_m;         // 1/m on the padded grid (single plane)
   const T* pz;            // sponge profile, rows
   const T* px;            // sponge profile, cols
@@ -387,6 +391,9 @@ constexpr int FL_VHIST = 4;   // ADJ: store v_n (adjoint_solve keep_v)
 constexpr int FL_GATHER = 8;  // FWD: receiver sampling blocks present
 constexpr int FL_BAND = 16;   // FWD: store u_n on the sponge frame; ADJ: reverse-
                               // reconstruct the forward and image against it
+constexpr int FL_ADJ3 = 64;   // ADJ (one-step kernels): three-level adjoint
+                              // V_{n-1} = coef (L V_n + R^T y_n) + 2d V_n - d^2 V_{n+1}
+                              // over the two V buffers (no w state; see k_step)
 constexpr int FL_LOCK = 32;   // FWD: lock-step Born pair in one launch -- the
                               // background step (second field set, point source,
                               // optional history) feeds its a0_n to the
@@ -403,6 +410,9 @@ template <typename T, bool ADJ, int FL>
 __host__ __device__ constexpr int step_min_blocks() {
   // (fp64 dual stages are 154 KB: one CTA per SM)
   // (counts for 256-thread CTAs; SG_TY < 8 builds smaller CTAs, more per SM)
+#ifdef SG_ADJ_CTAS
+  if (sizeof(T) == 4 && ADJ && !step_dual<ADJ, FL>()) return SG_ADJ_CTAS;
+#endif
   return (8 / kTY) * (sizeof(T) != 4 ? (step_dual<ADJ, FL>() ? 1 : 2)
                                      : (step_dual<ADJ, FL>() ? 2 : (ADJ ? SG_ADJ_MINB : SG_FP32_MINB)));
 }
@@ -778,9 +788,19 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
               lp = P::make(l0, l1);
             }
           }
-          const P so = P::fma(dd[q], sv, lp);
-          put(sout + q * ldx, so);
-          put(fout + q * ldx, P::fma(dd[q], ucs, ((dt2p * im[q]) * dd[q]) * so));
+          if constexpr ((FL & FL_ADJ3) != 0) {
+            // three-level form of the reference's exact transpose
+            // (seisopt/wavesim.py:330-345: lam_n = L v_n + 2 d lam_{n+1}
+            // - d^2 lam_{n+2} + R^T y_n, v_n = coef lam_{n+1}) in V = coef lam:
+            //   V_{n-1} = coef (L V_n + R^T y_n) + d (2 V_n - d V_{n+1});
+            // sv is V_{n+1} (the tile of f[cur ^ 1], overwritten in place)
+            const P cf = (dt2p * im[q]) * dd[q];
+            put(fout + q * ldx, P::fma(cf, lp, dd[q] * ((ucs + ucs) - dd[q] * sv)));
+          } else {
+            const P so = P::fma(dd[q], sv, lp);
+            put(sout + q * ldx, so);
+            put(fout + q * ldx, P::fma(dd[q], ucs, ((dt2p * im[q]) * dd[q]) * so));
+          }
           T v0, v1;
           ucs.split(v0, v1);
           if (LOAD_HIST) {

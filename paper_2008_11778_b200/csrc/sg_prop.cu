@@ -626,7 +626,14 @@ void launch_step_r(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a) {
   const int fl = (a.hist_on ? FL_HIST : 0) | (a.gsrc ? FL_GSRC : 0) |
                  (a.vhist ? FL_VHIST : 0) | (a.gather ? FL_GATHER : 0) | (a.band ? FL_BAND : 0);
   if constexpr (ADJ) {
-    if (fl & FL_BAND) launch_step_f<T, R, ADJ, FL_BAND>(h, s, a);
+    if (fl & FL_BAND) {
+      if (a.adj3) launch_step_f<T, R, ADJ, FL_BAND | FL_ADJ3>(h, s, a);
+      else launch_step_f<T, R, ADJ, FL_BAND>(h, s, a);
+    } else if (a.adj3) {
+      if (fl & FL_VHIST) launch_step_f<T, R, ADJ, FL_VHIST | FL_ADJ3>(h, s, a);
+      else if (fl & FL_HIST) launch_step_f<T, R, ADJ, FL_HIST | FL_ADJ3>(h, s, a);
+      else launch_step_f<T, R, ADJ, FL_ADJ3>(h, s, a);
+    }
     else if (fl & FL_VHIST) launch_step_f<T, R, ADJ, FL_VHIST>(h, s, a);
     else if (fl & FL_HIST) launch_step_f<T, R, ADJ, FL_HIST>(h, s, a);
     else launch_step_f<T, R, ADJ, 0>(h, s, a);
@@ -908,6 +915,10 @@ int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, con
   void* W1 = use2 ? h->w2 : h->w;  // one-step kernel: state in place
   StepArgs<T> a;
   SG_TRY(step_args<T>(h, a, h->l0, h->l1, h->w, W1, p.hist.base, p.hist.shots * p.hist.steps));
+  // one-step sweeps (also the boundary-saving fused reverse + adjoint step)
+  // run the three-level adjoint: 12 instead of 16 B per cell-update, no w
+  // buffer traffic; the opt-in two-step kernel keeps the V/w form
+  a.adj3 = (SG_ADJ3 && !use2) ? 1 : 0;
   a.count = count;
   a.s0 = s0;
   a.g0 = s0;  // groups of the first s0 shots use at most s0 image planes
@@ -981,6 +992,7 @@ int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, con
       }
       if (a.hist_on) a.hist_slot = p.hist.slot(n);
       a.vhist = p.vhist ? reinterpret_cast<T*>(p.vhist) + (int64_t)n * h->hplane : nullptr;
+      if (a.adj3) a.s_tile = a.f_tile[cur ^ 1];  // V_{n+1}, overwritten with V_{n-1}
       launch_step<T, true>(h, s, a);
       n -= 1;
     }

@@ -577,7 +577,14 @@ def test_c3_fp32_aa_misfit_curve_vs_fp64():
 def test_two_step_kernel_matches_one_step(order, recon):
     """fp32: the temporally blocked kernel (two steps per launch, ring
     recomputation, in-tile receivers) reproduces one-step launches: forward
-    data bit for bit, images/gradients to summation-order round-off."""
+    data bit for bit; images/gradients to fp32 round-off (the one-step
+    adjoint runs the three-level recurrence, the two-step kernel the V/w
+    increment form: same transpose, different rounding), and both Born
+    images to the fp64 reference within the fp32 tolerance.  (The fp32
+    gradient of this tiny case sits at ~1.2e-4 from the fp64 golden with
+    either adjoint form -- residual cancellation in the forward data,
+    tools/adj3_err.py, profiles/r01e_adj3_err.log -- so it is compared
+    between the kernels only.)"""
     _, wavesim = _api()
     case = small_case(order, True)
     g = case["gold"]
@@ -595,10 +602,12 @@ def test_two_step_kernel_matches_one_step(order, recon):
     (s1, v1, g1, i1, l1, lg1), (s2, v2, g2, i2, l2, lg2) = out
     assert torch.equal(s1, s2)
     assert v1 == v2
-    assert rel(g2.cpu().numpy(), g1.cpu().numpy()) <= 1e-6
-    assert rel(i2.cpu().numpy(), i1.cpu().numpy()) <= 1e-6
+    assert rel(g2.cpu().numpy(), g1.cpu().numpy()) <= 1e-5
+    assert rel(i2.cpu().numpy(), i1.cpu().numpy()) <= 1e-5
     assert abs(l1 - l2) <= 1e-6 * abs(l1)
-    assert rel(lg2.cpu().numpy(), lg1.cpu().numpy()) <= 1e-6
+    assert rel(lg2.cpu().numpy(), lg1.cpu().numpy()) <= 1e-5
+    for im in (i1, i2):
+        assert rel(im.cpu().numpy(), g["img"]) <= F32
 
 
 @pytest.mark.parametrize("recon", ["full", "checkpoint"])
@@ -712,9 +721,10 @@ def test_partial_born_cache(monkeypatch):
 def test_resident_sweeps_match_one_step():
     """fp32 cluster-resident whole-sweep kernels (opt-in, desc.resident=1):
     gathers / misfit bitwise those of the one-step kernels (same arithmetic
-    per cell), gradients and Born images to summation-order round-off (per-shot
-    instead of per-group image planes), and the fp32 gradient within the
-    north-star tolerance of the fp64 reference golden."""
+    per cell), gradients and Born images to fp32 round-off (per-shot instead
+    of per-group image planes; the resident adjoint keeps the V/w increment
+    form, the one-step kernel runs the three-level recurrence), and the fp32
+    gradient within the north-star tolerance of the fp64 reference golden."""
     _, wavesim = _api()
     case = c1(8)
     g = case["gold"]
@@ -737,10 +747,11 @@ def test_resident_sweeps_match_one_step():
     (s0, m0, v0, g0, i0), (s1, m1, v1, g1, i1) = out
     assert torch.equal(s0, s1)
     assert m0 == m1 and v0 == v1
-    assert rel(g1.cpu().numpy(), g0.cpu().numpy()) <= 1e-6
-    assert rel(i1.cpu().numpy(), i0.cpu().numpy()) <= 1e-6
+    assert rel(g1.cpu().numpy(), g0.cpu().numpy()) <= 1e-5
+    assert rel(i1.cpu().numpy(), i0.cpu().numpy()) <= 1e-5
     assert abs(v1 - float(g["value"])) <= F32 * float(g["value"])
     assert rel(g1.cpu().numpy(), g["grad"]) <= F32
+    assert rel(g0.cpu().numpy(), g["grad"]) <= F32
 
 
 def _replay_window(g, qr):
