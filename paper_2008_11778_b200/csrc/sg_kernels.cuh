@@ -413,6 +413,9 @@ __host__ __device__ constexpr int step_min_blocks() {
 #ifdef SG_ADJ_CTAS
   if (sizeof(T) == 4 && ADJ && !step_dual<ADJ, FL>()) return SG_ADJ_CTAS;
 #endif
+#ifdef SG_FWD_CTAS
+  if (sizeof(T) == 4 && !ADJ && !step_dual<ADJ, FL>()) return SG_FWD_CTAS;
+#endif
   return (8 / kTY) * (sizeof(T) != 4 ? (step_dual<ADJ, FL>() ? 1 : 2)
                                      : (step_dual<ADJ, FL>() ? 2 : (ADJ ? SG_ADJ_MINB : SG_FP32_MINB)));
 }
