@@ -73,6 +73,9 @@ constexpr int kHalo = 4;
 #ifndef SG_ADJ3
 #define SG_ADJ3 1  // three-level one-step adjoint (FL_ADJ3); 0 = V/w increment form
 #endif
+#ifndef SG_REV3
+#define SG_REV3 0  // three-level reverse forward in the boundary-saving kernel (FL_REV3)
+#endif
 #ifndef SG_EARLY_TMA
 #define SG_EARLY_TMA 1
 #endif
@@ -95,6 +98,7 @@ struct StepArgs {
   T* state;               // inc (forward) / w (adjoint), updated in place
   int cur;                // read f[cur], write f[cur ^ 1]
   int adj3;               // host: dispatch the FL_ADJ3 adjoint (s_tile = f_tile[cur ^ 1])
+  int rev3;               // host: dispatch FL_REV3 (r_stile = u tile of rf[rcur ^ 1])
   const T* inv_m;         // 1/m on the padded grid (single plane)
   const T* pz;            // sponge profile, rows
   const T* px;            // sponge profile, cols
@@ -394,6 +398,9 @@ constexpr int FL_BAND = 16;   // FWD: store u_n on the sponge frame; ADJ: revers
 constexpr int FL_ADJ3 = 64;   // ADJ (one-step kernels): three-level adjoint
                               // V_{n-1} = coef (L V_n + R^T y_n) + 2d V_n - d^2 V_{n+1}
                               // over the two V buffers (no w state; see k_step)
+constexpr int FL_REV3 = 128;  // ADJ with FL_BAND: three-level reverse forward
+                              // u_{n-1} = 2u_n + dt^2 a_n - u_{n+1} (interior;
+                              // frame from the band store), in place over u_{n+1}
 constexpr int FL_LOCK = 32;   // FWD: lock-step Born pair in one launch -- the
                               // background step (second field set, point source,
                               // optional history) feeds its a0_n to the
@@ -728,9 +735,15 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
             if (!FULL && q >= nq) continue;
             const P acc = accel(lap2(colu, scu, q), q);
             accs[q] = acc;
-            const P incn = lds2(sinc + q * kBX) - dt2p * acc;
-            put(rsout + q * ldx, incn);
-            P um1 = colu[q + R] - incn;
+            P um1;
+            if constexpr ((FL & FL_REV3) != 0) {
+              // three-level reversal: the stage's state tile is u_{n+1}
+              um1 = P::fma(dt2p, acc, (colu[q + R] + colu[q + R]) - lds2(sinc + q * kBX));
+            } else {
+              const P incn = lds2(sinc + q * kBX) - dt2p * acc;
+              put(rsout + q * ldx, incn);
+              um1 = colu[q + R] - incn;
+            }
             if (bsrc != nullptr && tile_band) {
               int bi0, bi1;
               band2(q, bi0, bi1);

@@ -627,7 +627,8 @@ void launch_step_r(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a) {
                  (a.vhist ? FL_VHIST : 0) | (a.gather ? FL_GATHER : 0) | (a.band ? FL_BAND : 0);
   if constexpr (ADJ) {
     if (fl & FL_BAND) {
-      if (a.adj3) launch_step_f<T, R, ADJ, FL_BAND | FL_ADJ3>(h, s, a);
+      if (a.adj3 && a.rev3) launch_step_f<T, R, ADJ, FL_BAND | FL_ADJ3 | FL_REV3>(h, s, a);
+      else if (a.adj3) launch_step_f<T, R, ADJ, FL_BAND | FL_ADJ3>(h, s, a);
       else launch_step_f<T, R, ADJ, FL_BAND>(h, s, a);
     } else if (a.adj3) {
       if (fl & FL_VHIST) launch_step_f<T, R, ADJ, FL_VHIST | FL_ADJ3>(h, s, a);
@@ -928,17 +929,25 @@ int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, con
   const bool img_on = a.hist_on || p.band_recon;
   a.image = img_on ? reinterpret_cast<T*>(h->img) : nullptr;
   int rcur = p.rcur0;
+  CUtensorMap utile[2];  // REV3: u_{n+1} tiles of u0 / u1
   if (p.band_recon) {
     constexpr int R8 = 4, R2 = 1;
     if (h->d.order == 8) {
       SG_TRY((get_map<T, R8>(h, h->u0, MAP_HALO, h->B, &a.r_halo[0])));
       SG_TRY((get_map<T, R8>(h, h->u1, MAP_HALO, h->B, &a.r_halo[1])));
       SG_TRY((get_map<T, R8>(h, h->inc, MAP_TILE, h->B, &a.r_stile)));
+      SG_TRY((get_map<T, R8>(h, h->u0, MAP_TILE, h->B, &utile[0])));
+      SG_TRY((get_map<T, R8>(h, h->u1, MAP_TILE, h->B, &utile[1])));
     } else {
       SG_TRY((get_map<T, R2>(h, h->u0, MAP_HALO, h->B, &a.r_halo[0])));
       SG_TRY((get_map<T, R2>(h, h->u1, MAP_HALO, h->B, &a.r_halo[1])));
       SG_TRY((get_map<T, R2>(h, h->inc, MAP_TILE, h->B, &a.r_stile)));
+      SG_TRY((get_map<T, R2>(h, h->u0, MAP_TILE, h->B, &utile[0])));
+      SG_TRY((get_map<T, R2>(h, h->u1, MAP_TILE, h->B, &utile[1])));
     }
+    // three-level reversal (the sweep starts from u_{nt-1} in rf[rcur0] and
+    // u_nt in rf[rcur0 ^ 1], k_band_init)
+    a.rev3 = (a.adj3 && SG_REV3) ? 1 : 0;
     a.rf[0] = field<T>(h->u0, h);
     a.rf[1] = field<T>(h->u1, h);
     a.rstate = field<T>(h->inc, h);
@@ -986,6 +995,7 @@ int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, con
       if (img_on) a.image = reinterpret_cast<T*>(h->img) + (int64_t)(SG_IMG_PARITY ? cur : 0) * h->B * h->hplane;
       if (p.band_recon) {
         a.rcur = rcur;
+        if (a.rev3) a.r_stile = utile[rcur ^ 1];
         a.amp = (T)h->wavelet[n];
         a.band_slot = n - 1;  // u_{n-1} on the frame (none below step 0)
         rcur ^= 1;
