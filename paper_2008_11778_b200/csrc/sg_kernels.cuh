@@ -74,7 +74,7 @@ constexpr int kHalo = 4;
 #define SG_ADJ3 1  // three-level one-step adjoint (FL_ADJ3); 0 = V/w increment form
 #endif
 #ifndef SG_REV3
-#define SG_REV3 0  // three-level reverse forward in the boundary-saving kernel (FL_REV3)
+#define SG_REV3 1  // three-level reverse forward in the boundary-saving kernel (FL_REV3)
 #endif
 #ifndef SG_EARLY_TMA
 #define SG_EARLY_TMA 1
