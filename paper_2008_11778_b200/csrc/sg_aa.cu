@@ -76,10 +76,16 @@ struct Vec<double> {
 // Windows of up to 12 columns load every column of an element before the
 // stores (kHoist, 2 CTAs/SM for the registers): C2 push 0.70 -> 0.55 ms
 // (5.1 -> 6.5 TB/s); wider windows keep the load-after-store order at 4 CTAs/SM.
+// Windows wider than 12 columns keep 4 CTAs/SM: 2 CTAs/SM removes their
+// accumulator spills but was slower (m = 20 push 2.01 vs 1.27 ms,
+// profiles/r01e_ab_aa_wide.log).
+#ifndef SG_AA_WIDE_MINB
+#define SG_AA_WIDE_MINB 4
+#endif
 template <int MW, bool VEC>
 struct PushCfg {
   static constexpr bool kHoist = VEC && MW <= 12;
-  static constexpr int kMinBlocks = kHoist ? 2 : 4;
+  static constexpr int kMinBlocks = kHoist ? 2 : (MW > 12 ? SG_AA_WIDE_MINB : 4);
 };
 
 template <typename T, int MW, bool VEC>
@@ -736,6 +742,7 @@ int push_t(sg_aa* a, const void* p, const void* g) {
   else if (mw <= 8) PUSH(8);
   else if (mw <= 12) PUSH(12);
   else if (mw <= 16) PUSH(16);
+  else if (mw <= 20) PUSH(20);  // BASELINE C5 window (m = 20)
   else PUSH(32);
 #undef PUSH
   k_sum_cols<<<na, 256, 0, a->stream>>>(a->part, nb, na, a->out);
@@ -800,6 +807,7 @@ int step_t(sg_aa* a, double beta, const double* gamma, void* out) {
   else if (mw <= 8) STEP(8);
   else if (mw <= 12) STEP(12);
   else if (mw <= 16) STEP(16);
+  else if (mw <= 20) STEP(20);
   else STEP(32);
 #undef STEP
   count_launch();

@@ -11,7 +11,8 @@ sys.path.insert(0, ROOT)
 def main():
     import torch
     from paper_2008_11778_b200 import anderson
-    n, m = 50_000_000, 10
+    n = 50_000_000
+    m = int(sys.argv[1]) if len(sys.argv) > 1 else 10
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(0)
     vecs = [(torch.randn(n, generator=g, device=dev), torch.randn(n, generator=g, device=dev))
