@@ -76,6 +76,9 @@ constexpr int kHalo = 4;
 #ifndef SG_REV3
 #define SG_REV3 1  // three-level reverse forward in the boundary-saving kernel (FL_REV3)
 #endif
+#ifndef SG_ADJ_GMAX
+#define SG_ADJ_GMAX 4  // largest shot group of the one-step fp32 adjoint
+#endif
 #ifndef SG_EARLY_TMA
 #define SG_EARLY_TMA 1
 #endif

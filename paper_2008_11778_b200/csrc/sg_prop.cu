@@ -480,10 +480,6 @@ int group_for(const sg_handle* h, int count, int per_sm = 0) {
   return best;
 }
 
-int ngroups(const sg_handle* h, int count, int per_sm = 0) {
-  const int G = group_for(h, count, per_sm);
-  return (count + G - 1) / G;
-}
 
 // TMA descriptors.  Guarded buffers (fields, state) are viewed as 3-D
 // {ldx, nzp + 2 kGuard, B} starting after the lead row; histories as
@@ -603,10 +599,15 @@ void launch_step_f(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a0) {
   }
   StepArgs<T> a = a0;
   a.G = group_for(h, a.count, per_sm);
+  // one-step fp32 adjoint: at most SG_ADJ_GMAX shots per CTA group (C3: 4
+  // instead of the cost model's 5 -- adjoint step 14.1 -> 13.3 us,
+  // profiles/r01e_ab_group2.log)
+  if (sizeof(T) == 4 && ADJ && !step_dual<ADJ, FL>() && h->d.group <= 0)
+    a.G = std::min(a.G, SG_ADJ_GMAX);
   a.rec_blocks = (a.G * h->d.n_rec + RB - 1) / RB;
   const int extra = (!ADJ && (FL & FL_GATHER)) ? a.rec_blocks : 0;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(h->ntiles + extra, ngroups(h, a.count, per_sm));
+  cfg.gridDim = dim3(h->ntiles + extra, (a.count + a.G - 1) / a.G);
   cfg.blockDim = dim3(kTX, kTY);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
