@@ -7,11 +7,16 @@ Workload (default, BASELINE.json configs[2] = "C3"): one complete FWI gradient
 per step -- 30 shots, 201x601 grid (241x641 padded), nt 4000, 8th-order
 stencil, fp32, 20-cell sponge: forward sweep with history store, residual +
 misfit, adjoint sweep with fused imaging, image reduction, fold, and (N > 1)
-one all-reduce.  Shots are sharded over the N ranks in contiguous blocks.
-C3/C4 scale weakly (each rank owns the config's shot count; the survey has
-30*N / 60*N evenly spaced shots); C5 is the fixed 240-shot survey split over
-the ranks (strong); --scaling overrides.  Synthetic seeded layered-fault model (the paper's Marmousi
-is not available offline).
+one all-reduce.  Shots are sharded over the N ranks in contiguous blocks
+(SURVEY s8e): every config is its fixed BASELINE survey split over the ranks
+(strong scaling: C3 30 -> 4,4,4,4,4,4,3,3 at N = 8, C5 240 -> 30 each);
+--scaling weak gives every rank the config's full shot count instead.
+Synthetic seeded layered-fault model (the paper's Marmousi is not available
+offline).
+
+The C3 line also carries ``c5_kernels``: the two boundary-saving step kernels
+of C5 (band-storing forward, fused reverse-forward + adjoint) timed on the
+full 1041 x 3041 padded grid over 8-shot launches -- the HBM-bound case.
 
 metric: Gcell-updates/s = 2 * shots * nt * padded cells per gradient (forward +
 adjoint stencil sweeps; recompute sweeps of checkpoint mode are not counted)
@@ -58,6 +63,78 @@ def peaks():
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
     except Exception:
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+class NvmlClockSampler:
+    """SM clocks + throttle reasons through NVML (nvidia_ml_py) every 20 ms
+    during the timed region."""
+
+    # nvmlClocksEventReason* bits
+    BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+            "sw_power_cap": 0x4}
+
+    def __init__(self, index):
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+                fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                rs = fn(self.h)
+                ut = nv.nvmlDeviceGetUtilizationRates(self.h).gpu
+                self.rows.append((sm, mx, rs, ut))
+            except Exception:
+                pass
+            self._stop.wait(0.02)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        loaded = [r[0] for r in self.rows if r[3] >= 50] or [r[0] for r in self.rows]
+        reasons = sorted({k for r in self.rows for k, b in self.BITS.items() if r[2] & b})
+        counts = {k: sum(1 for r in self.rows if r[2] & b) for k, b in self.BITS.items()}
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml",
+                "reason_samples": {k: v for k, v in counts.items() if v}}
+
+
+def clock_sampler(index):
+    try:
+        return NvmlClockSampler(index)
+    except Exception:
+        return ClockSampler(index)
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 class ClockSampler:
@@ -132,12 +209,12 @@ BASE_SHOTS = {"c1": 5, "c3": 30, "c4": 60, "c5": 240}
 
 
 def scaling_mode(args):
-    """C3/C4: weak (each rank owns the config's full shot set, the survey grows
-    with N).  C5 is quoted as a fixed 240-shot survey sharded over 1..8 GPUs
-    (strong); C1 is a parity case (strong, replicas of 5 shots)."""
+    """Strong by default: the config's fixed survey (BASELINE.json) sharded
+    over the ranks in contiguous blocks.  --scaling weak: every
+    rank owns the config's shot count (a survey of shots * N)."""
     if args.scaling != "auto":
         return args.scaling
-    return "weak" if args.config in ("c3", "c4") else "strong"
+    return "strong"
 
 
 def total_shots(args, world):
@@ -197,7 +274,7 @@ def run_reference(args):
             "data": "synthetic",
             "config": {"workload": workload_name(args.config), "sample": sample},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": sample},
+                             "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -232,6 +309,7 @@ def run_reference_c2(args):
                       "config": {"workload": "C2 standalone AA mixing step", "sample": sample},
                       "cpu_baseline": {"value": v, "unit": "ms/iteration",
                                        "cores": os.cpu_count() or 1, "kind": "port",
+                                       "cpu_model": cpu_model(),
                                        "sample": sample},
                       "e2e": {"value": v, "unit": "ms/iteration", "h2d_bytes_per_step": 0,
                               "d2h_bytes_per_step": 0}}), flush=True)
@@ -282,7 +360,7 @@ def run_lsrtm(args):
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = _lib.launch_count()
-    with ClockSampler(local) as clk:
+    with clock_sampler(local) as clk:
         barrier()
         e0.record()
         for _ in range(args.steps):
@@ -295,7 +373,18 @@ def run_lsrtm(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     C = padded_cells(case)
-    cells = 3.0 * S * nt * C  # background + scattered + adjoint sweeps per gradient
+    # value counts the reference algorithm's stencil updates per LSRTM
+    # gradient (BornKernel with every background cached,
+    # seisopt/gradients.py:177-220): Born forward + adjoint = 2 sweeps per
+    # shot.  Shots whose background is not cached here run extra sweeps
+    # (lock-step background, and in CHECKPOINT / BOUNDARY mode its re-run in
+    # the adjoint); those are reported as executed_gcell_per_s.
+    nloc = kern._range()[1]
+    cached = kern.cached
+    recon = kern.ws.query()["recon"]
+    per_uncached = 3 if recon == "full" else 4
+    cells = 2.0 * S * nt * C
+    executed = (2.0 * cached + per_uncached * (nloc - cached)) * nt * C * world
     p_host = np.zeros(grid.nz * grid.nx)
     obj.value_and_grad(p_host)  # untimed: the host path's first-use allocations
     barrier()
@@ -318,6 +407,8 @@ def run_lsrtm(args):
                        "recon": q["recon"], "shots_per_launch": q["batch"],
                        "cached_background": kern.cached},
             "gradients_per_s": args.steps / (ms / 1e3), "misfit": val,
+            "executed_gcell_per_s": executed * args.steps / (ms / 1e3) / 1e9,
+            "sweeps_per_shot": {"cached": 2, "uncached": per_uncached},
             "e2e": {"value": cells * args.steps / e2e_s / 1e9, "unit": UNIT,
                     "h2d_bytes_per_step": p_host.nbytes, "d2h_bytes_per_step": p_host.nbytes + 8},
             "gpu_launches": launches, "clocks": clk.summary(), "cpu_baseline": None}),
@@ -327,22 +418,88 @@ def run_lsrtm(args):
     return 0
 
 
+def init_dist(dev, world):
+    """NCCL process group (world > 1) with NCCL's init log on, so the
+    communicator size each rank reports can be checked against WORLD_SIZE."""
+    import torch.distributed as dist
+    if world <= 1:
+        return None
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    dist.init_process_group("nccl", device_id=dev)
+    return dist
+
+
+def shard_report(dist, world, shard, n_shots):
+    """Every rank's (first shot, count) and the communicator size."""
+    import torch
+    s0, cnt = (shard.shot0, shard.count) if shard else (0, n_shots)
+    if dist is None:
+        return {"backend": None, "comm_nranks": 1, "shot_ranges": [[s0, cnt]]}
+    t = torch.tensor([s0, cnt], dtype=torch.int64, device="cuda")
+    allt = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(allt, t)
+    return {"backend": dist.get_backend(), "comm_nranks": dist.get_world_size(),
+            "shot_ranges": [[int(x[0]), int(x[1])] for x in allt]}
+
+
+def c5_kernel_record(dev, peak, peak_src, reps=400, shots=8, nt=400):
+    """BASELINE C5's boundary-saving step kernels on the full 1001 x 3001 grid
+    (1041 x 3041 padded), `shots`-shot launches as the C5 gradient runs them
+    (two concurrent chains): the band-storing forward and the fused
+    reverse-forward + three-level adjoint with imaging, CUDA events over
+    `reps` launches on the handle's stream.  nt only sizes the band store
+    (the per-step work does not depend on it).  Algorithmic bytes per SURVEY
+    s8d (stencil update 16 B, imaging 12 B per shot-cell); DRAM bytes from the
+    committed ncu capture of the same kernels (profiles/traffic.json)."""
+    from paper_2008_11778_b200 import synthetic
+    from paper_2008_11778_b200.wavesim import Propagator
+    case = synthetic.layered_case("c5", n_shots=shots, nt=nt)
+    prop = Propagator(case["grid"], case["geometry"], case["wavelet"], case["config"],
+                      dtype="float32", device=dev, recon="boundary")
+    try:
+        prop.set_model(case["init"].m)
+        C = prop.shape[0] * prop.shape[1]
+        es = 4
+        ms_fwd = prop.time_step_kernel(6, shots, reps=reps)
+        ms_adj = prop.time_step_kernel(5, shots, reps=reps)
+    finally:
+        prop.close()
+    tr = {}
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        tr = json.load(open(tpath)).get("c5", {})
+    out = {"grid": "1041x3041 padded (C5)", "shots_per_launch": shots, "reps": reps,
+           "peak": peak, "peak_source": peak_src}
+    for name, ms, alg_b in (("forward_band_step", ms_fwd, 4 * es),
+                            ("reverse_adjoint_step", ms_adj, 8 * es + 3 * es)):
+        alg = shots * C * alg_b
+        dram = tr.get(name)
+        dram_step = dram * shots if (dram is not None and tr.get("per_shot")) else dram
+        out[name] = {
+            "ms_per_step": ms, "alg_bytes_per_shot_cell": alg_b,
+            "alg_gbs": alg / (ms / 1e3) / 1e9, "alg_frac": alg / (ms / 1e3) / 1e9 / peak,
+            "dram_bytes_per_step": dram_step,
+            "dram_gbs": (dram_step / (ms / 1e3) / 1e9) if dram_step else None,
+            "dram_frac": (dram_step / (ms / 1e3) / 1e9 / peak) if dram_step else None,
+        }
+    return out
+
+
 def run_ours(args):
     import torch
-    import torch.distributed as dist
 
     from paper_2008_11778_b200 import _lib, gradients, shards
-    from paper_2008_11778_b200.model import VelocityModel
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dist = init_dist(dev, world)
     case = build_case(args.config, total_shots(args, world))
     geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
     S, nt = geom.n_sources, geom.nt
     shard = shards.ShotShard.from_env(S) if world > 1 else None
+    comm = shard_report(dist, world, shard, S)
     # observed data: forward model of the true model on this rank's shots (untimed)
     from paper_2008_11778_b200.wavesim import Propagator
     tmp = Propagator(grid, geom, wav, cfg, dtype=case["dtype"], device=dev)
@@ -367,7 +524,7 @@ def run_ours(args):
     p_dev = torch.as_tensor(p_host, device=dev, dtype=obj.prop.tdtype)
 
     def barrier():
-        if world > 1:
+        if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -377,17 +534,22 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = _lib.launch_count()
-    with ClockSampler(local) as clk:
+    phases = {"forward": 0.0, "residual": 0.0, "adjoint": 0.0, "reduce": 0.0}
+    with clock_sampler(local) as clk:
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
             val, grad = obj.value_and_grad(p_dev)
+            # device time of this gradient's phases (events recorded on the
+            # handle's stream, read after the call's own synchronisation)
+            for k, v in obj.prop.phase_times().items():
+                phases[k] += v
         e1.record(stream)
         barrier()
     launches = _lib.launch_count() - l0
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     C = padded_cells(case)
@@ -406,51 +568,74 @@ def run_ours(args):
     barrier()
     e2e_s = time.perf_counter() - t0
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
+    if dist is not None:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_s = float(te.item())
     e2e_value = cells_per_grad * args.steps / e2e_s / 1e9
     nbytes = p_host.nbytes
 
-    # roofline of the dominant kernel (adjoint step + imaging), timed live with
-    # CUDA events on the launching stream; the step launches run as the sweep
-    # runs them (two concurrent half-batch chains), so the time is per step of
-    # the whole batch and the bytes those of all its shots
+    # Roofline of the dominant kernel.  Both step kernels launch nt times per
+    # gradient; their live per-step time is the gradient's phase time / nt
+    # (CUDA events on the launching stream around the captured sweep graphs,
+    # a step = the whole batch as two concurrent half-batch chains), and the
+    # dominant one is the phase with the larger share of the gradient.
     prop = obj.prop
     local_shots = shard.count if shard else S
     es = prop.esz
     q = prop.query()
-    launch_shots = min(local_shots, q["batch"])         # shots per step launch
-    reps = 100 if launch_shots * C < 2e7 else 20
+    launch_shots = min(local_shots, q["batch"])
+    batches = -(-local_shots // launch_shots)
+    steps_run = args.steps * nt * batches
+    ms_fwd = phases["forward"] / steps_run
+    ms_adj = phases["adjoint"] / steps_run
+    total_ph = sum(phases.values())
     if q["recon"] == "boundary":
         # band-storing forward (stencil 4s; the sponge-frame store is <6 % of
         # cells, not counted) and the fused reverse-forward + adjoint step
         # (two stencil updates 8s + imaging 3s)
-        ms_fwd = prop.time_step_kernel(6, launch_shots, reps=reps)
-        ms_adj = prop.time_step_kernel(5, launch_shots, reps=reps)
         bytes_fwd = launch_shots * C * (4 * es)
         bytes_adj = launch_shots * C * (8 * es + 3 * es)
         names = ("forward_band_step", "reverse_adjoint_step")
+        iso = (6, 5)
     else:
-        ms_fwd = prop.time_step_kernel(0, launch_shots, reps=reps)
-        ms_adj = prop.time_step_kernel(1, launch_shots, reps=reps)
         bytes_fwd = launch_shots * C * (4 * es + es)       # stencil 4s + history store s
         bytes_adj = launch_shots * C * (4 * es + 3 * es)   # stencil 4s + imaging 3s
         names = ("forward_step", "adjoint_step")
+        iso = (0, 1)
+    if q["recon"] == "checkpoint":
+        # the adjoint phase also re-runs the forward per segment
+        bytes_adj += launch_shots * C * (4 * es + es)
+    reps = 100 if launch_shots * C < 2e7 else 20
+    iso_fwd = prop.time_step_kernel(iso[0], launch_shots, reps=reps)
+    iso_adj = prop.time_step_kernel(iso[1], launch_shots, reps=reps)
     peak, peak_src = peaks()
-    dom = (names[1], ms_adj, bytes_adj) if ms_adj * 1.0 >= ms_fwd else \
-        (names[0], ms_fwd, bytes_fwd)
-    achieved = dom[2] / (dom[1] / 1e3) / 1e9
-    traffic = None
+    kern = {}
+    traffic_tab = {}
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            tr = json.load(open(tpath)).get(args.config, {})
-            traffic = tr.get(dom[0])
-            if traffic is not None and tr.get("per_shot"):
-                traffic *= launch_shots
+            traffic_tab = json.load(open(tpath)).get(args.config, {})
         except Exception:
-            traffic = None
+            traffic_tab = {}
+    for name, msk, byt, ph, iso_ms in ((names[0], ms_fwd, bytes_fwd, phases["forward"], iso_fwd),
+                                       (names[1], ms_adj, bytes_adj, phases["adjoint"], iso_adj)):
+        tr = traffic_tab.get(name)
+        if tr is not None and traffic_tab.get("per_shot"):
+            tr *= launch_shots
+        kern[name] = {"ms_per_step": msk, "share": ph / total_ph if total_ph else None,
+                      "bytes_per_step": byt, "achieved": byt / (msk / 1e3) / 1e9,
+                      "frac": byt / (msk / 1e3) / 1e9 / peak, "traffic": tr,
+                      "traffic_gbs": (tr / (msk / 1e3) / 1e9) if tr else None,
+                      "isolated_ms_per_step": iso_ms}
+    dom = max(names, key=lambda n: kern[n]["share"] or 0.0)
+    dk = kern[dom]
+
+    c5 = None
+    if args.config == "c3" and rank == 0 and not args.no_c5_kernels:
+        try:
+            c5 = c5_kernel_record(dev, peak, peak_src)
+        except Exception as exc:  # recorded, not fatal for the C3 line
+            c5 = {"error": f"{type(exc).__name__}: {exc}"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -459,6 +644,7 @@ def run_ours(args):
         nts = {"c1": 800, "c3": 250, "c4": 150, "c5": 20}.get(args.config, 200)
         dt, cells = cpu_sample(case, cores, shots, nts)
         cpu = {"value": cells / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
+               "cpu_model": cpu_model(),
                "sample": f"oracle fwi_gradient, {shots} shots x {nts} steps of the same grid, "
                          f"threads={cores}, {dt:.1f} s"}
     if rank == 0:
@@ -483,24 +669,30 @@ def run_ours(args):
                        "l2": l2},
             "gradients_per_s": grads_per_s,
             "misfit": val,
+            "comm": comm,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes,
                     "d2h_bytes_per_step": nbytes + 8, "gradients_per_s": args.steps / e2e_s},
-            "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved,
+            "phases_ms_per_gradient": {k: v / args.steps for k, v in phases.items()},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": dk["achieved"],
                          "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": dk["frac"], "traffic": dk["traffic"],
                          # ncu DRAM bytes of the step / its live time: the HBM
                          # actually moved (C3 fields stay in L2, so < achieved)
-                         "traffic_gbs": (traffic / (dom[1] / 1e3) / 1e9) if traffic else None,
+                         "traffic_gbs": dk["traffic_gbs"],
+                         "traffic_frac": (dk["traffic_gbs"] / peak) if dk["traffic_gbs"] else None,
                          "shots_per_step": launch_shots,
                          "chains": prop.chains(launch_shots),
-                         "bytes_per_step": dom[2], "ms_per_step": dom[1],
-                         "forward_ms_per_step": ms_fwd, "adjoint_ms_per_step": ms_adj},
+                         "bytes_per_step": dk["bytes_per_step"], "ms_per_step": dk["ms_per_step"],
+                         "share": dk["share"], "timing": "gradient phase events / steps",
+                         "kernels": kern},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
+        if c5 is not None:
+            line["c5_kernels"] = c5
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
     return 0
@@ -551,7 +743,7 @@ def run_c2(args):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = _lib.launch_count()
-    with ClockSampler(local) as clk:
+    with clock_sampler(local) as clk:
         e0.record()
         for k in range(m + 1 + args.warmup, total):
             win.push(*stream[k])
@@ -592,6 +784,7 @@ def run_c2(args):
             oracle.aa_step(wo, 1.0, oracle.aa_weights(wo))
         cms = (time.perf_counter() - t0) * 1e3 / 2 * (n / nc)
         cpu = {"value": cms, "unit": "ms/iteration", "cores": os.cpu_count() or 1,
+               "cpu_model": cpu_model(),
                "kind": "port", "sample": f"oracle AAWindow push+weights+step at N={nc}, m={m}, "
                                          "2 steady-state iterations, scaled x10 to N=5e7"}
     line = {"metric": "AA mixing step time (push + weights + step)", "value": ms,
@@ -621,9 +814,11 @@ def main():
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c5-kernels", action="store_true",
+                    help="skip the C5 boundary-saving kernel record of the C3 line")
     ap.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"],
-                    help="weak: config shot count per rank (C3/C4 default); "
-                         "strong: config shot count sharded over ranks (C1/C5 default)")
+                    help="strong (default): the config's survey sharded over the ranks; "
+                         "weak: the config's shot count on every rank")
     args = ap.parse_args()
     if args.config == "c2":
         return run_c2(args) if args.impl != "reference" else run_reference_c2(args)

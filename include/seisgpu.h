@@ -93,6 +93,12 @@ typedef struct sg_aa sg_aa;
 
 const char* sg_last_error(void);
 int sg_version(void);
+/* Build options compiled into this library: SG_BUILD_EXPERIMENTAL = the
+ * opt-in two-step (desc.step_mode = 2) and cluster-resident (desc.resident)
+ * kernels, measured slower than the one-step kernels on B200 and left out of
+ * the default build (-DSG_EXPERIMENTAL=1 adds them). */
+#define SG_BUILD_EXPERIMENTAL 1
+int sg_build_flags(void);
 
 /* ---- propagator context: replaces seisopt.wavesim.Workspace
  *      (seisopt/wavesim.py:183-214), built once per geometry rather than per
@@ -166,6 +172,12 @@ int sg_born_adjoint(sg_handle* h, int32_t shot0, int32_t count, const void* data
 int sg_lsrtm_gradient(sg_handle* h, int32_t shot0, int32_t count, const void* m_r_dev,
                       const void* d_r_dev, double* value_host, void* grad_dev,
                       int32_t accumulate);
+/* LSRTM objective value only: *value_host = 1/2 ||L m_r - d_r||^2 over shots
+ * [shot0, shot0+count) (LsrtmObjective.value / residual_norm,
+ * seisopt/gradients.py:351-369) -- Born forward with the residual reduced in
+ * fp64 on the device; no Born data leave it.  Synchronises. */
+int sg_lsrtm_misfit(sg_handle* h, int32_t shot0, int32_t count, const void* m_r_dev,
+                    const void* d_r_dev, double* value_host);
 
 /* Single-shot forward with the full acceleration history returned
  * (forward_solve with keep_history, seisopt/wavesim.py:354-378):
@@ -195,6 +207,12 @@ int sg_resident_plan(sg_handle* h, int32_t* out);
  * (sg_chains concurrent chains); *ms_per_launch = mean time per step. */
 int sg_time_step_kernel(sg_handle* h, int32_t which, int32_t count, int32_t reps,
                         float* ms_per_launch);
+
+/* Device time of the phases of the last sg_fwi_gradient call, summed over
+ * its shot batches (CUDA events on the handle's stream): ms_out[4] = {forward
+ * sweep, residual + injection, adjoint sweep with imaging, image reduction}.
+ * Synchronises on the recorded events. */
+int sg_phase_times(sg_handle* h, float* ms_out);
 
 /* Number of kernel launches this handle (or AA window) has issued. */
 int64_t sg_launch_count(void);
@@ -248,6 +266,19 @@ int sg_vec_blend_dots(int64_t n, int32_t dtype, const void* g, const void* p,
                       void* cuda_stream);
 int sg_vec_stats(int64_t n, int32_t dtype, const void* x, double* out_host,
                  void* cuda_stream);
+
+/* Krylov / quasi-Newton vector kernels (seisopt/krylov.py:130-190 Arnoldi
+ * projections and updates, seisopt/optim/quasi_newton.py:36-55 two-loop
+ * recursion), one pass over k <= 32 device vectors of `dtype`, length n;
+ * xs is a HOST array of k device pointers.
+ *  sg_vec_multi_dot  : out_host[i] = <x_i, y> (i < k), out_host[k] = <y, y>
+ *                      (fp64 accumulation, fixed-order block sums)
+ *  sg_vec_multi_axpy : z = y + sum_i coef_host[i] x_i (y may be NULL: z = sum),
+ *                      fp64 per element; z may alias y or one of the x_i */
+int sg_vec_multi_dot(int64_t n, int32_t dtype, int32_t k, const void* const* xs,
+                     const void* y, double* out_host, void* cuda_stream);
+int sg_vec_multi_axpy(int64_t n, int32_t dtype, int32_t k, const double* coef_host,
+                      const void* const* xs, const void* y, void* z, void* cuda_stream);
 
 #ifdef __cplusplus
 }

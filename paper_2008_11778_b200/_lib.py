@@ -20,6 +20,7 @@ SG_OK, SG_ERR_ARG, SG_ERR_STABILITY, SG_ERR_EMPTY = 0, 1, 2, 3
 SG_ERR_CUDA, SG_ERR_OOM, SG_ERR_MODEL, SG_ERR_STATE = 4, 5, 6, 7
 SG_F32, SG_F64 = 4, 8
 SG_RECON_FULL, SG_RECON_CHECKPOINT, SG_RECON_AUTO, SG_RECON_BOUNDARY = 0, 1, 2, 3
+SG_BUILD_EXPERIMENTAL = 1
 
 
 class EmptyWindowError(Exception):
@@ -60,6 +61,7 @@ _IP = C.POINTER(C.c_int32)
 SIGNATURES = {
     "sg_last_error": (C.c_char_p, []),
     "sg_version": (C.c_int, []),
+    "sg_build_flags": (C.c_int, []),
     "sg_create": (C.c_int, [C.POINTER(SgDesc), C.POINTER(_P)]),
     "sg_destroy": (C.c_int, [_P]),
     "sg_set_stream": (C.c_int, [_P, _P]),
@@ -75,12 +77,14 @@ SIGNATURES = {
     "sg_born_forward": (C.c_int, [_P, _I32, _I32, _P, _P]),
     "sg_born_adjoint": (C.c_int, [_P, _I32, _I32, _P, _P, _I32]),
     "sg_lsrtm_gradient": (C.c_int, [_P, _I32, _I32, _P, _P, _DP, _P, _I32]),
+    "sg_lsrtm_misfit": (C.c_int, [_P, _I32, _I32, _P, _P, _DP]),
     "sg_forward_history": (C.c_int, [_P, _I32, _P, _P]),
     "sg_adjoint_history": (C.c_int, [_P, _P, _P]),
     "sg_query": (C.c_int, [_P, _IP, _IP, _DP]),
     "sg_chains": (C.c_int, [_P, C.c_int32]),
     "sg_resident_plan": (C.c_int, [_P, _IP]),
     "sg_time_step_kernel": (C.c_int, [_P, _I32, _I32, _I32, C.POINTER(C.c_float)]),
+    "sg_phase_times": (C.c_int, [_P, C.POINTER(C.c_float)]),
     "sg_launch_count": (C.c_int64, []),
     "sg_aa_create": (C.c_int, [_I64, _I32, _I32, _I32, C.POINTER(_P)]),
     "sg_aa_destroy": (C.c_int, [_P]),
@@ -97,6 +101,8 @@ SIGNATURES = {
     "sg_vec_lerp": (C.c_int, [_I64, _I32, _P, _P, _D, _P, _P]),
     "sg_vec_blend_dots": (C.c_int, [_I64, _I32, _P, _P, _P, _P, _DP, _P]),
     "sg_vec_stats": (C.c_int, [_I64, _I32, _P, _DP, _P]),
+    "sg_vec_multi_dot": (C.c_int, [_I64, _I32, _I32, C.POINTER(_P), _P, _DP, _P]),
+    "sg_vec_multi_axpy": (C.c_int, [_I64, _I32, _I32, _DP, C.POINTER(_P), _P, _P, _P]),
 }
 
 _lock = threading.Lock()
@@ -143,6 +149,12 @@ def check(rc: int, what: str = ""):
     if rc == SG_ERR_MODEL:
         raise ModelError(msg)
     raise SeisGpuError(f"[code {rc}] {msg}")
+
+
+def experimental_kernels() -> bool:
+    """Whether the opt-in two-step / cluster-resident kernels are compiled in
+    (build with defines=("SG_EXPERIMENTAL=1",))."""
+    return bool(load().sg_build_flags() & SG_BUILD_EXPERIMENTAL)
 
 
 def launch_count() -> int:

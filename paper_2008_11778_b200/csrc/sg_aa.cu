@@ -425,6 +425,83 @@ __global__ void k_stats(int64_t n, const T* __restrict__ x, double* __restrict__
   }
 }
 
+// Krylov / quasi-Newton vector kernels (seisopt/krylov.py:130-190,
+// seisopt/optim/quasi_newton.py:36-55): one pass over k vectors x_i and y.
+struct Ptrs {
+  const void* p[kMaxMem];
+};
+
+// partials per block: <x_i, y> (i < k), then <y, y>; fp64 accumulation
+template <typename T, int MW>
+__global__ void __launch_bounds__(kThreads)
+    k_multi_dot(int64_t n, int k, const Ptrs xs, const T* __restrict__ y,
+                double* __restrict__ part) {
+  double acc[MW];
+#pragma unroll
+  for (int i = 0; i < MW; ++i) acc[i] = 0.0;
+  double yy = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double yv = (double)y[e];
+#pragma unroll
+    for (int i = 0; i < MW; ++i)
+      if (i < k) acc[i] += (double)reinterpret_cast<const T*>(xs.p[i])[e] * yv;
+    yy += yv * yv;
+  }
+  const int na = k + 1;
+  __shared__ double red[kThreads / 32][kMaxMem + 2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  auto warp_put = [&](int idx, double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[wid][idx] = v;
+  };
+#pragma unroll
+  for (int i = 0; i < MW; ++i)
+    if (i < k) warp_put(i, acc[i]);
+  warp_put(k, yy);
+  __syncthreads();
+  for (int q = threadIdx.x; q < na; q += blockDim.x) {
+    double sum = 0.0;
+    for (int w2 = 0; w2 < kThreads / 32; ++w2) sum += red[w2][q];
+    part[(int64_t)blockIdx.x * na + q] = sum;
+  }
+}
+
+// z = y + sum_i c_i x_i (y == nullptr: z = sum_i c_i x_i), fp64 arithmetic
+// per element, in the order y, x_0, x_1, ... (krylov.py:189, quasi_newton.py:44-54)
+template <typename T, int MW>
+__global__ void __launch_bounds__(kThreads)
+    k_multi_axpy(int64_t n, int k, const Coefs c, const Ptrs xs, const T* y, T* z) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double acc = y ? (double)y[e] : 0.0;
+#pragma unroll
+    for (int i = 0; i < MW; ++i)
+      if (i < k) acc += c.c[i] * (double)reinterpret_cast<const T*>(xs.p[i])[e];
+    z[e] = (T)acc;
+  }
+}
+
+// ||f_k - sum_i gamma_i DF_i||^2 partials (the explicit combined residual of
+// qr.py:89-95 for Gram-solved windows), fp64 per element
+template <typename T, int MW>
+__global__ void __launch_bounds__(kThreads)
+    k_aa_resid(const T* __restrict__ fk, const T* __restrict__ DF, int64_t n, int64_t ld,
+               const Slots slots, int nw, const Coefs gam, double* __restrict__ part) {
+  double acc = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double r = (double)fk[e];
+#pragma unroll
+    for (int i = 0; i < MW; ++i)
+      if (i < nw) r -= gam.c[i] * (double)DF[(int64_t)slots.s[i] * ld + e];
+    acc += r * r;
+  }
+  const double s = block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(kBlocks, (n + kThreads - 1) / kThreads)); }
@@ -527,6 +604,10 @@ void drop_oldest(sg_aa* a) {
 // device QR instead.
 bool cholesky(const sg_aa* a, std::vector<double>& R, std::vector<double>& diag) {
   const int k = a->ncols, m = a->memory;
+  // fp64 (parity) windows leave the Gram path already at rho / ||a|| <= 1e-3:
+  // the normal equations carry ~cond^2 eps error, and the reference solves
+  // through its QR (qr.py:82-87); fp32 windows keep the Gram down to 1e-5
+  const double unres = a->esz == 8 ? 1e-6 : 1e-10;
   R.assign((size_t)k * k, 0.0);
   diag.assign(k, 0.0);
   bool unresolved = false;
@@ -541,7 +622,7 @@ bool cholesky(const sg_aa* a, std::vector<double>& R, std::vector<double>& diag)
     for (int l = 0; l < j; ++l) s -= R[(size_t)l * k + j] * R[(size_t)l * k + j];
     const double nrm = std::sqrt(std::max(ajj, 0.0));
     double rho = s > 0.0 ? std::sqrt(s) : 0.0;
-    if (s <= 1e-10 * ajj) unresolved = true;
+    if (s <= unres * ajj) unresolved = true;
     if (rho <= 1e-300 || rho < 1e-15 * std::max(nrm, 1.0) || s <= 1e-14 * ajj) rho = 0.0;
     diag[j] = rho;
     R[(size_t)j * k + j] = rho;
@@ -659,6 +740,35 @@ int qr_solve(sg_aa* a, std::vector<double>& gmm, double& resid) {
   return SG_OK;
 }
 
+// ||f_k - DF gamma|| by one device pass over the window (fp64 accumulation)
+template <typename T>
+int explicit_resid(sg_aa* a, const std::vector<double>& gmm, double& out) {
+  const int k = a->ncols;
+  const int nb = grid_for(a->n);
+  Slots sl{};
+  Coefs cf{};
+  for (int i = 0; i < k; ++i) {
+    sl.s[i] = slot_of(a, i);
+    cf.c[i] = gmm[i];
+  }
+  const T* fk = reinterpret_cast<const T*>(a->fk);
+  const T* DF = reinterpret_cast<const T*>(a->DF);
+#define RES(MW) k_aa_resid<T, MW><<<nb, kThreads, 0, a->stream>>>(fk, DF, a->n, a->ld, sl, k, cf, a->part)
+  if (k <= 4) RES(4);
+  else if (k <= 8) RES(8);
+  else if (k <= 16) RES(16);
+  else RES(32);
+#undef RES
+  k_sum_cols<<<1, 256, 0, a->stream>>>(a->part, nb, 1, a->out);
+  count_launch(2);
+  SG_CK(cudaGetLastError());
+  double r2 = 0.0;
+  SG_CK(cudaMemcpyAsync(&r2, a->out, sizeof(double), cudaMemcpyDeviceToHost, a->stream));
+  SG_CK(cudaStreamSynchronize(a->stream));
+  out = std::sqrt(std::max(r2, 0.0));
+  return SG_OK;
+}
+
 int compute_weights(sg_aa* a) {
   const int k = a->ncols;
   if (k == 0 || a->pushes < 2) return fail(SG_ERR_EMPTY, "aa_weights needs at least one stored difference");
@@ -684,6 +794,13 @@ int compute_weights(sg_aa* a) {
     for (double v : y) y2 += v * v;
     const double r2 = std::max(a->fk2 - y2, 0.0);
     a->resid = std::min(std::sqrt(r2), std::sqrt(a->fk2));
+    // fp64 (parity) mode: the explicit ||f - A gamma|| instead of the
+    // cancellation-prone sqrt(||f||^2 - ||y||^2) (accurate to ~sqrt(eps) ||f||)
+    if (a->esz == 8) {
+      double r = 0.0;
+      SG_TRY(explicit_resid<double>(a, gmm, r));
+      a->resid = std::min(r, std::sqrt(a->fk2));
+    }
   }
   // alpha recovery with fsum fix-up (anderson.py:41-52)
   std::vector<double> al(k + 1);
@@ -982,6 +1099,76 @@ int sg_vec_blend_dots(int64_t n, int32_t dtype, const void* g, const void* p, co
   }
   out[0] = s0;
   out[1] = s1;
+  return SG_OK;
+}
+
+int sg_vec_multi_dot(int64_t n, int32_t dtype, int32_t k, const void* const* xs, const void* y,
+                     double* out, void* stream) {
+  if (n < 1 || k < 0 || k > kMaxMem || (k > 0 && !xs) || !y || !out)
+    return fail(SG_ERR_ARG, "bad arguments");
+  if (dtype != SG_F32 && dtype != SG_F64) return fail(SG_ERR_ARG, "dtype must be SG_F32 or SG_F64");
+  Ptrs px{};
+  for (int i = 0; i < k; ++i) {
+    if (!xs[i]) return fail(SG_ERR_ARG, "null vector");
+    px.p[i] = xs[i];
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int nb = grid_for(n), na = k + 1;
+  double* part = nullptr;
+  SG_CK(cudaMallocAsync((void**)&part, sizeof(double) * ((size_t)na * nb + na), s));
+  double* dout = part + (size_t)na * nb;
+#define MD(TT, MW) k_multi_dot<TT, MW><<<nb, kThreads, 0, s>>>(n, k, px, (const TT*)y, part)
+#define MDT(TT)                  \
+  do {                           \
+    if (k <= 1) MD(TT, 1);       \
+    else if (k <= 4) MD(TT, 4);  \
+    else if (k <= 8) MD(TT, 8);  \
+    else if (k <= 16) MD(TT, 16); \
+    else MD(TT, 32);             \
+  } while (0)
+  if (dtype == SG_F32) MDT(float);
+  else MDT(double);
+#undef MDT
+#undef MD
+  k_sum_cols<<<na, 256, 0, s>>>(part, nb, na, dout);
+  count_launch(2);
+  SG_CK(cudaGetLastError());
+  SG_CK(cudaMemcpyAsync(out, dout, na * sizeof(double), cudaMemcpyDeviceToHost, s));
+  SG_CK(cudaFreeAsync(part, s));
+  SG_CK(cudaStreamSynchronize(s));
+  return SG_OK;
+}
+
+int sg_vec_multi_axpy(int64_t n, int32_t dtype, int32_t k, const double* coef,
+                      const void* const* xs, const void* y, void* z, void* stream) {
+  if (n < 0 || k < 0 || k > kMaxMem || (k > 0 && (!xs || !coef)) || !z)
+    return fail(SG_ERR_ARG, "bad arguments");
+  if (dtype != SG_F32 && dtype != SG_F64) return fail(SG_ERR_ARG, "dtype must be SG_F32 or SG_F64");
+  if (n == 0) return SG_OK;
+  Ptrs px{};
+  Coefs cf{};
+  for (int i = 0; i < k; ++i) {
+    if (!xs[i]) return fail(SG_ERR_ARG, "null vector");
+    px.p[i] = xs[i];
+    cf.c[i] = coef[i];
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int nb = grid_for(n);
+#define MA(TT, MW) k_multi_axpy<TT, MW><<<nb, kThreads, 0, s>>>(n, k, cf, px, (const TT*)y, (TT*)z)
+#define MAT(TT)                  \
+  do {                           \
+    if (k <= 1) MA(TT, 1);       \
+    else if (k <= 4) MA(TT, 4);  \
+    else if (k <= 8) MA(TT, 8);  \
+    else if (k <= 16) MA(TT, 16); \
+    else MA(TT, 32);             \
+  } while (0)
+  if (dtype == SG_F32) MAT(float);
+  else MAT(double);
+#undef MAT
+#undef MA
+  count_launch();
+  SG_CK(cudaGetLastError());
   return SG_OK;
 }
 

@@ -24,6 +24,13 @@
 #include "seisgpu.h"
 #include "sg_common.cuh"
 #include "sg_kernels.cuh"
+// The two-step (k_step2) and cluster-resident (k_resident) kernels were
+// measured slower than k_step on B200.  Their types stay
+// visible, but the kernels are only instantiated with -DSG_EXPERIMENTAL=1
+// (tools/ builds); the product library ships the kernels that won their A/B.
+#ifndef SG_EXPERIMENTAL
+#define SG_EXPERIMENTAL 0
+#endif
 #include "sg_kernels2.cuh"
 #include "sg_resident.cuh"
 
@@ -116,6 +123,7 @@ __global__ void k_model_stats(const M* __restrict__ m, int64_t n, double* __rest
 //   mode 0 (FWI):  ybar = (w_t dt)(f - g), acc w_t (f-g)^2   (seisopt/gradients.py:137-147)
 //   mode 1 (LSRTM): ybar = f - g,          acc (f-g)^2       (seisopt/gradients.py:269-273)
 //   mode 2 (value): no ybar,               acc w_t (f-g)^2   (seisopt/gradients.py:70-79)
+//   mode 3 (LSRTM value): no ybar,         acc (f-g)^2       (seisopt/gradients.py:363-369)
 template <typename T>
 __global__ void k_residual(const T* __restrict__ f, const T* __restrict__ g, T* ybar,
                            int64_t rows, int nt, int nrec, double dt, int mode,
@@ -127,7 +135,7 @@ __global__ void k_residual(const T* __restrict__ f, const T* __restrict__ g, T* 
   const int64_t r1 = min(rows, r0 + per);
   for (int64_t row = r0; row < r1; ++row) {
     const int n = (int)(row % nt);
-    const double w = (mode == 1) ? 1.0 : ((n == 0 || n == nt - 1) ? 0.5 : 1.0);
+    const double w = (mode == 1 || mode == 3) ? 1.0 : ((n == 0 || n == nt - 1) ? 0.5 : 1.0);
     const T wdt = (T)(w * dt);
     const int64_t base = row * nrec;
     double racc = 0.0;
@@ -304,6 +312,11 @@ struct sg_handle {
   int born_b0 = -1, born_count = 0;
 
   std::map<std::string, GraphEntry> graphs;
+
+  // phase events of the last sg_fwi_gradient call: 5 per batch (forward sweep
+  // | residual + injection | adjoint sweep | image reduction), read lazily
+  std::vector<cudaEvent_t> ph_ev;
+  int ph_batches = 0;
 
   // cluster-resident whole-sweep kernels (sg_resident.cuh)
   std::vector<int> rec_rows_h, rec_cols_h;  // receiver taps (4, n_rec), host copy
@@ -588,14 +601,16 @@ int step_args(sg_handle* h, StepArgs<T>& a, void* F0, void* F1, void* S0, void* 
 }
 
 template <typename T, int R, bool ADJ, int FL>
-void launch_step_f(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a0) {
-  static bool attr = false;
+int launch_step_f(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a0) {
+  // the shared-memory attribute is per device: one bit per ordinal
+  static std::atomic<uint64_t> attr_devs{0};
   constexpr int smem = step_smem_bytes<T, R, ADJ, step_dual<ADJ, FL>()>();
   constexpr int per_sm = step_min_blocks<T, ADJ, FL>();
-  if (!attr) {
-    cudaFuncSetAttribute(k_step<T, R, ADJ, FL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         smem);
-    attr = true;
+  const uint64_t bit = 1ull << (h->d.device & 63);
+  if (!(attr_devs.load() & bit)) {
+    SG_CK(cudaFuncSetAttribute(k_step<T, R, ADJ, FL>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_devs.fetch_or(bit);
   }
   StepArgs<T> a = a0;
   a.G = group_for(h, a.count, per_sm);
@@ -618,54 +633,55 @@ void launch_step_f(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a0) {
     cfg.attrs = attr_pdl;
     cfg.numAttrs = 1;
   }
-  cudaLaunchKernelEx(&cfg, k_step<T, R, ADJ, FL>, a);
+  SG_CK(cudaLaunchKernelEx(&cfg, k_step<T, R, ADJ, FL>, a));
   count_launch();
+  return SG_OK;
 }
 
 template <typename T, int R, bool ADJ>
-void launch_step_r(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a) {
+int launch_step_r(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a) {
   const int fl = (a.hist_on ? FL_HIST : 0) | (a.gsrc ? FL_GSRC : 0) |
                  (a.vhist ? FL_VHIST : 0) | (a.gather ? FL_GATHER : 0) | (a.band ? FL_BAND : 0);
   if constexpr (ADJ) {
     if (fl & FL_BAND) {
-      if (a.adj3 && a.rev3) launch_step_f<T, R, ADJ, FL_BAND | FL_ADJ3 | FL_REV3>(h, s, a);
-      else if (a.adj3) launch_step_f<T, R, ADJ, FL_BAND | FL_ADJ3>(h, s, a);
-      else launch_step_f<T, R, ADJ, FL_BAND>(h, s, a);
+      if (a.adj3 && a.rev3) return launch_step_f<T, R, ADJ, FL_BAND | FL_ADJ3 | FL_REV3>(h, s, a);
+      else if (a.adj3) return launch_step_f<T, R, ADJ, FL_BAND | FL_ADJ3>(h, s, a);
+      else return launch_step_f<T, R, ADJ, FL_BAND>(h, s, a);
     } else if (a.adj3) {
-      if (fl & FL_VHIST) launch_step_f<T, R, ADJ, FL_VHIST | FL_ADJ3>(h, s, a);
-      else if (fl & FL_HIST) launch_step_f<T, R, ADJ, FL_HIST | FL_ADJ3>(h, s, a);
-      else launch_step_f<T, R, ADJ, FL_ADJ3>(h, s, a);
+      if (fl & FL_VHIST) return launch_step_f<T, R, ADJ, FL_VHIST | FL_ADJ3>(h, s, a);
+      else if (fl & FL_HIST) return launch_step_f<T, R, ADJ, FL_HIST | FL_ADJ3>(h, s, a);
+      else return launch_step_f<T, R, ADJ, FL_ADJ3>(h, s, a);
     }
-    else if (fl & FL_VHIST) launch_step_f<T, R, ADJ, FL_VHIST>(h, s, a);
-    else if (fl & FL_HIST) launch_step_f<T, R, ADJ, FL_HIST>(h, s, a);
-    else launch_step_f<T, R, ADJ, 0>(h, s, a);
+    else if (fl & FL_VHIST) return launch_step_f<T, R, ADJ, FL_VHIST>(h, s, a);
+    else if (fl & FL_HIST) return launch_step_f<T, R, ADJ, FL_HIST>(h, s, a);
+    else return launch_step_f<T, R, ADJ, 0>(h, s, a);
   } else if (a.rstate != nullptr) {
     // fused lock-step Born pair (scattered gathers; background history optional)
-    if (fl & FL_HIST) launch_step_f<T, R, ADJ, FL_LOCK | FL_GATHER | FL_HIST>(h, s, a);
-    else launch_step_f<T, R, ADJ, FL_LOCK | FL_GATHER>(h, s, a);
+    if (fl & FL_HIST) return launch_step_f<T, R, ADJ, FL_LOCK | FL_GATHER | FL_HIST>(h, s, a);
+    else return launch_step_f<T, R, ADJ, FL_LOCK | FL_GATHER>(h, s, a);
   } else if (fl & FL_BAND) {
     // band-saving forwards: FWI gradient (gathers) and Born background (one-slot history)
-    if (fl & FL_HIST) launch_step_f<T, R, ADJ, FL_BAND | FL_HIST>(h, s, a);
-    else if (fl & FL_GATHER) launch_step_f<T, R, ADJ, FL_BAND | FL_GATHER>(h, s, a);
-    else launch_step_f<T, R, ADJ, FL_BAND>(h, s, a);
+    if (fl & FL_HIST) return launch_step_f<T, R, ADJ, FL_BAND | FL_HIST>(h, s, a);
+    else if (fl & FL_GATHER) return launch_step_f<T, R, ADJ, FL_BAND | FL_GATHER>(h, s, a);
+    else return launch_step_f<T, R, ADJ, FL_BAND>(h, s, a);
   } else {
   switch (fl & (FL_HIST | FL_GSRC | FL_GATHER)) {
-    case 0: launch_step_f<T, R, ADJ, 0>(h, s, a); break;
-    case FL_HIST: launch_step_f<T, R, ADJ, FL_HIST>(h, s, a); break;
-    case FL_GATHER: launch_step_f<T, R, ADJ, FL_GATHER>(h, s, a); break;
-    case FL_HIST | FL_GATHER: launch_step_f<T, R, ADJ, FL_HIST | FL_GATHER>(h, s, a); break;
-    case FL_GSRC: launch_step_f<T, R, ADJ, FL_GSRC>(h, s, a); break;
-    case FL_GSRC | FL_GATHER: launch_step_f<T, R, ADJ, FL_GSRC | FL_GATHER>(h, s, a); break;
-    case FL_GSRC | FL_HIST: launch_step_f<T, R, ADJ, FL_GSRC | FL_HIST>(h, s, a); break;
-    default: launch_step_f<T, R, ADJ, FL_GSRC | FL_HIST | FL_GATHER>(h, s, a); break;
+    case 0: return launch_step_f<T, R, ADJ, 0>(h, s, a);
+    case FL_HIST: return launch_step_f<T, R, ADJ, FL_HIST>(h, s, a);
+    case FL_GATHER: return launch_step_f<T, R, ADJ, FL_GATHER>(h, s, a);
+    case FL_HIST | FL_GATHER: return launch_step_f<T, R, ADJ, FL_HIST | FL_GATHER>(h, s, a);
+    case FL_GSRC: return launch_step_f<T, R, ADJ, FL_GSRC>(h, s, a);
+    case FL_GSRC | FL_GATHER: return launch_step_f<T, R, ADJ, FL_GSRC | FL_GATHER>(h, s, a);
+    case FL_GSRC | FL_HIST: return launch_step_f<T, R, ADJ, FL_GSRC | FL_HIST>(h, s, a);
+    default: return launch_step_f<T, R, ADJ, FL_GSRC | FL_HIST | FL_GATHER>(h, s, a);
   }
   }
 }
 
 template <typename T, bool ADJ>
-void launch_step(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a) {
-  if (h->d.order == 8) launch_step_r<T, 4, ADJ>(h, s, a);
-  else launch_step_r<T, 1, ADJ>(h, s, a);
+int launch_step(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a) {
+  if (h->d.order == 8) return launch_step_r<T, 4, ADJ>(h, s, a);
+  return launch_step_r<T, 1, ADJ>(h, s, a);
 }
 
 // ---- sweep pieces (enqueue only) --------------------------------------------
@@ -708,7 +724,9 @@ struct FwdPlan {
 // two-step (temporally blocked) kernels: fp32 only, no Born grid source, no
 // v-history.  Opt-in (desc.step_mode == 2): measured slower than the one-step
 // kernel on B200 at C3 and C5 (profiles/r01_step_kernels_by_config.txt).
-bool two_step_ok(const sg_handle* h) { return h->esz == 4 && h->d.step_mode == 2; }
+bool two_step_ok(const sg_handle* h) {
+  return SG_EXPERIMENTAL && h->esz == 4 && h->d.step_mode == 2;
+}
 
 template <typename T>
 int step2_args(sg_handle* h, Step2Args<T>& a, void* F0, void* F1, void* S0, void* S1,
@@ -801,7 +819,7 @@ void launch_step2(const sg_handle* h, cudaStream_t s, const Step2Args<float>& a)
 
 template <typename T>
 void launch_step2_t(const sg_handle* h, cudaStream_t s, const Step2Args<T>& a, bool adj) {
-  if constexpr (sizeof(T) == 4) {
+  if constexpr (sizeof(T) == 4 && SG_EXPERIMENTAL) {
     if (adj) launch_step2<true>(h, s, a);
     else launch_step2<false>(h, s, a);
   }
@@ -890,7 +908,7 @@ int enq_forward(sg_handle* h, cudaStream_t s, int count, int n0, int n1, const F
         a.gsrc = reinterpret_cast<const T*>(p.gsrc) + (int64_t)(n - p.gsrc_n0) * h->hplane;
       a.gather = p.gathers ? reinterpret_cast<T*>(h->gath) + (int64_t)n * h->d.n_rec : nullptr;
       a.band_slot = n;
-      launch_step<T, false>(h, s, a);
+      SG_TRY((launch_step<T, false>(h, s, a)));
       n += 1;
     }
     cur ^= 1;
@@ -1004,7 +1022,7 @@ int enq_adjoint(sg_handle* h, cudaStream_t s, int count, int n_hi, int n_lo, con
       if (a.hist_on) a.hist_slot = p.hist.slot(n);
       a.vhist = p.vhist ? reinterpret_cast<T*>(p.vhist) + (int64_t)n * h->hplane : nullptr;
       if (a.adj3) a.s_tile = a.f_tile[cur ^ 1];  // V_{n+1}, overwritten with V_{n-1}
-      launch_step<T, true>(h, s, a);
+      SG_TRY((launch_step<T, true>(h, s, a)));
       n -= 1;
     }
     cur ^= 1;
@@ -1060,7 +1078,7 @@ int enq_lockstep(sg_handle* h, cudaStream_t s, int count, int n0, int n1, const 
     a.amp = (T)h->wavelet[n];
     if (a.hist_on) a.hist_slot = hist.slot(n);
     a.gather = reinterpret_cast<T*>(h->gath) + (int64_t)n * h->d.n_rec;
-    launch_step<T, false>(h, s, a);
+    SG_TRY((launch_step<T, false>(h, s, a)));
     cur ^= 1;
   }
   return SG_OK;
@@ -1209,7 +1227,7 @@ int residual(sg_handle* h, int cnt, const T* obs, int mode) {
   k_residual<T><<<blocks, 256, 0, h->stream>>>(reinterpret_cast<const T*>(h->gath), obs,
                                                reinterpret_cast<T*>(h->gath), rows, h->d.nt,
                                                h->d.n_rec, h->d.dt, mode, h->part);
-  const double scale = (mode == 1) ? 0.5 : 0.5 * h->d.dt;
+  const double scale = (mode == 1 || mode == 3) ? 0.5 : 0.5 * h->d.dt;
   k_finish_sum<<<1, 1024, 0, h->stream>>>(h->part, blocks, scale, h->scal);
   count_launch(2);
   SG_CK(cudaGetLastError());
@@ -1265,7 +1283,7 @@ bool res_enabled(const sg_handle* h) {
   // opt-in: measured slower than the one-step kernels on B200 at C1/C3
   // (cluster waves leave a third of the SMs idle, 1 CTA/SM)
   const int want = env != 0 ? env : h->d.resident;
-  return h->esz == 4 && want > 0 && h->d.step_mode != 2;
+  return SG_EXPERIMENTAL && h->esz == 4 && want > 0 && h->d.step_mode != 2;
 }
 
 template <typename T, int R>
@@ -1378,7 +1396,7 @@ int res_plan_r(sg_handle* h) {
 // whether this handle's sweeps run as resident launches (plans on first use)
 template <typename T>
 bool res_ready(sg_handle* h) {
-  if constexpr (sizeof(T) != 4) {
+  if constexpr (sizeof(T) != 4 || !SG_EXPERIMENTAL) {
     return false;
   } else {
     if (!res_enabled(h)) return false;
@@ -1454,8 +1472,8 @@ int launch_res_f(const sg_handle* h, cudaStream_t s, const ResArgs<T>& a, int cn
 template <typename T>
 int enq_res_forward(sg_handle* h, cudaStream_t s, int cnt, const HistRef& hr, bool gathers,
                     int s0 = 0) {
-  if constexpr (sizeof(T) != 4) {
-    return fail(SG_ERR_STATE, "resident sweeps are fp32 only");
+  if constexpr (sizeof(T) != 4 || !SG_EXPERIMENTAL) {
+    return fail(SG_ERR_STATE, "resident sweeps: fp32 and -DSG_EXPERIMENTAL=1 only");
   } else {
   ResArgs<T> a;
   res_common<T>(h, a, cnt);
@@ -1493,8 +1511,8 @@ int enq_res_forward(sg_handle* h, cudaStream_t s, int cnt, const HistRef& hr, bo
 // R^T y from the dense band array; per-shot images into h->img planes [0, B)
 template <typename T>
 int enq_res_adjoint(sg_handle* h, cudaStream_t s, int cnt, const HistRef& hr, int s0 = 0) {
-  if constexpr (sizeof(T) != 4) {
-    return fail(SG_ERR_STATE, "resident sweeps are fp32 only");
+  if constexpr (sizeof(T) != 4 || !SG_EXPERIMENTAL) {
+    return fail(SG_ERR_STATE, "resident sweeps: fp32 and -DSG_EXPERIMENTAL=1 only");
   } else {
   ResArgs<T> a;
   res_common<T>(h, a, cnt);
@@ -1735,31 +1753,36 @@ int fwi_gradient_t(sg_handle* h, int shot0, int count, const void* obs, double* 
   SG_CK(cudaMemsetAsync(h->scal, 0, sizeof(double), h->stream));
   SG_CK(cudaMemsetAsync(h->acc_img, 0, (size_t)h->hplane * h->esz, h->stream));
   const size_t per = (size_t)h->d.nt * h->d.n_rec * h->esz;
-  // optional phase timing (env SG_PHASE_TIMING=1): forward / glue / adjoint
+  // phase events per batch (sg_phase_times; printed with SG_PHASE_TIMING=1)
   static const bool timing = getenv("SG_PHASE_TIMING") != nullptr;
-  cudaEvent_t ev[5] = {};
-  if (timing)
-    for (auto& e : ev) cudaEventCreate(&e);
+  h->ph_batches = 0;
   for (int b0 = shot0; b0 < shot0 + count; b0 += h->B) {
     const int cnt = std::min(h->B, shot0 + count - b0);
-    if (timing) cudaEventRecord(ev[0], h->stream);
+    while ((int)h->ph_ev.size() < 5 * (h->ph_batches + 1)) {
+      cudaEvent_t e;
+      SG_CK(cudaEventCreate(&e));
+      h->ph_ev.push_back(e);
+    }
+    cudaEvent_t* ev = h->ph_ev.data() + 5 * h->ph_batches;
+    h->ph_batches++;
+    SG_CK(cudaEventRecord(ev[0], h->stream));
     {
       Trace t_("forward sweep");
       SG_TRY(do_forward_batch<T>(h, b0, cnt, true));
     }
-    if (timing) cudaEventRecord(ev[1], h->stream);
+    SG_CK(cudaEventRecord(ev[1], h->stream));
     SG_TRY(residual<T>(h, cnt, reinterpret_cast<const T*>((const char*)obs + (b0 - shot0) * per),
                        0));
     SG_TRY(fill_injection<T>(h, cnt));
-    if (timing) cudaEventRecord(ev[2], h->stream);
+    SG_CK(cudaEventRecord(ev[2], h->stream));
     {
       Trace t_("adjoint sweep + imaging");
       SG_TRY(do_adjoint_batch<T>(h, cnt, nullptr, 0));
     }
-    if (timing) cudaEventRecord(ev[3], h->stream);
+    SG_CK(cudaEventRecord(ev[3], h->stream));
     SG_TRY(reduce_images<T>(h, cnt));
+    SG_CK(cudaEventRecord(ev[4], h->stream));
     if (timing) {
-      cudaEventRecord(ev[4], h->stream);
       cudaEventSynchronize(ev[4]);
       float t[4];
       for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
@@ -1767,8 +1790,6 @@ int fwi_gradient_t(sg_handle* h, int shot0, int count, const void* obs, double* 
               "adjoint %.3f ms, image reduce %.3f ms\n", b0, cnt, t[0], t[1], t[2], t[3]);
     }
   }
-  if (timing)
-    for (auto& e : ev) cudaEventDestroy(e);
   SG_TRY(fold_out<T>(h, grad, accumulate));
   if (misfit) {
     SG_CK(cudaMemcpyAsync(misfit, h->scal, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -1988,6 +2009,26 @@ int born_adjoint_core(sg_handle* h, int shot0, int count, const void* data, int 
   return SG_OK;
 }
 
+// LSRTM objective value J = 1/2 ||L m_r - d_r||^2 (LsrtmObjective.value,
+// seisopt/gradients.py:363-369): Born forward per batch and the fused fp64
+// residual reduction; the Born data never leave the device
+template <typename T>
+int lsrtm_misfit_t(sg_handle* h, int shot0, int count, const void* m_r, const void* d_r,
+                   double* value) {
+  SG_TRY(ensure_batch(h));
+  SG_CK(cudaMemsetAsync(h->scal, 0, sizeof(double), h->stream));
+  const size_t gper = (size_t)h->d.nt * h->d.n_rec * h->esz;
+  for (int b0 = shot0, cnt = 0; b0 < shot0 + count; b0 += cnt) {
+    cnt = born_next_batch(h, b0, shot0 + count);
+    SG_TRY(born_forward_t<T>(h, b0, cnt, m_r, h->gath));
+    SG_TRY(residual<T>(h, cnt, reinterpret_cast<const T*>((const char*)d_r + (b0 - shot0) * gper),
+                       3));
+  }
+  SG_CK(cudaMemcpyAsync(value, h->scal, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  SG_CK(cudaStreamSynchronize(h->stream));
+  return SG_OK;
+}
+
 // ---- single-shot history export (forward_solve / adjoint_solve) ----------------
 
 template <typename T>
@@ -2136,7 +2177,8 @@ int time_kernel_t(sg_handle* h, int which, int count, int reps, float* ms) {
 extern "C" {
 
 const char* sg_last_error(void) { return sg::g_err.c_str(); }
-int sg_version(void) { return 1; }
+int sg_version(void) { return 2; }
+int sg_build_flags(void) { return SG_EXPERIMENTAL ? SG_BUILD_EXPERIMENTAL : 0; }
 int64_t sg_launch_count(void) { return sg::g_launches.load(); }
 
 int sg_create(const sg_desc* d, sg_handle** out) {
@@ -2207,6 +2249,7 @@ int sg_destroy(sg_handle* h) {
     if (h->ev_join[c]) cudaEventDestroy(h->ev_join[c]);
   }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  for (auto e : h->ph_ev) cudaEventDestroy(e);
   delete h;
   return SG_OK;
 }
@@ -2500,6 +2543,15 @@ int sg_lsrtm_gradient(sg_handle* h, int32_t shot0, int32_t count, const void* m_
                      accumulate, m_r);
 }
 
+int sg_lsrtm_misfit(sg_handle* h, int32_t shot0, int32_t count, const void* m_r,
+                    const void* d_r, double* value) {
+  sg::Trace trace_("sg_lsrtm_misfit");
+  SG_TRY(check_handle(h));
+  SG_TRY(check_range(h, shot0, count));
+  if (!m_r || !d_r || !value) return fail(SG_ERR_ARG, "null argument");
+  return SG_DISPATCH(h, lsrtm_misfit_t, h, shot0, count, m_r, d_r, value);
+}
+
 int sg_forward_history(sg_handle* h, int32_t shot, void* gather, void* accel) {
   sg::Trace trace_("sg_forward_history");
   SG_TRY(check_handle(h));
@@ -2543,6 +2595,23 @@ int sg_resident_plan(sg_handle* h, int32_t* out) {
   out[3] = on ? h->res_threads : 0;
   out[4] = on ? h->res_clusters : 0;
   out[5] = on ? ResSmem<float>(true, h->res_SR, h->res_W, h->res_hrows, h->res_hboxes).bytes : 0;
+  return SG_OK;
+}
+
+int sg_phase_times(sg_handle* h, float* ms) {
+  if (!h || !ms) return fail(SG_ERR_ARG, "null argument");
+  if (h->ph_batches == 0) return fail(SG_ERR_STATE, "no gradient has run on this handle");
+  SG_CK(cudaSetDevice(h->d.device));
+  for (int k = 0; k < 4; ++k) ms[k] = 0.f;
+  for (int b = 0; b < h->ph_batches; ++b) {
+    cudaEvent_t* ev = h->ph_ev.data() + 5 * b;
+    SG_CK(cudaEventSynchronize(ev[4]));
+    for (int k = 0; k < 4; ++k) {
+      float t = 0.f;
+      SG_CK(cudaEventElapsedTime(&t, ev[k], ev[k + 1]));
+      ms[k] += t;
+    }
+  }
   return SG_OK;
 }
 

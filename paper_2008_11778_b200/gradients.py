@@ -109,8 +109,9 @@ def fwi_synthetic(model, wavelet, geometry, config=SimConfig(), threads=1, works
     is accepted for signature compatibility; all shots run batched on the GPU."""
     prop = workspace if isinstance(workspace, Propagator) else get_propagator(
         model.grid, geometry, wavelet, config, dtype, device)
-    prop.set_model(model.m)
-    return _gathers(prop.synthetic(), geometry.dt)
+    with prop._lock:  # set_model + sweep on a handle other threads may share
+        prop.set_model(model.m)
+        return _gathers(prop.synthetic(), geometry.dt)
 
 
 def fwi_gradient(model, observed, wavelet, geometry, config=SimConfig(), counters=None,
@@ -119,12 +120,13 @@ def fwi_gradient(model, observed, wavelet, geometry, config=SimConfig(), counter
     if len(observed) != geometry.n_sources:
         raise ValueError("observed data does not cover all sources")
     prop = get_propagator(model.grid, geometry, wavelet, config, dtype, device)
-    prop.set_model(model.m)
-    value, grad = prop.gradient(_stack(observed))
+    with prop._lock:
+        prop.set_model(model.m)
+        value, grad = prop.gradient(_stack(observed))
+        grad = grad.double().cpu().numpy()
     if counters is not None:
         counters.grad_evals += 1
-    return ObjectiveEval(value=float(value), gradient=grad.double().cpu().numpy(),
-                         gradient_eval_count_delta=1)
+    return ObjectiveEval(value=float(value), gradient=grad, gradient_eval_count_delta=1)
 
 
 class BornKernel:
@@ -324,26 +326,26 @@ class LsrtmObjective:
     def grid(self):
         return self.kernel.grid
 
-    def _resid(self, p):
+    def _half_sq(self, p):
+        """1/2 ||L m_r - d_r||^2 of this rank's shots (fused Born forward +
+        fp64 residual reduction, sg_lsrtm_misfit), summed over ranks."""
         torch = _torch()
-        syn = self.kernel.forward_device(p if isinstance(p, torch.Tensor) else
-                                         np.asarray(p, dtype=np.float64))
-        return syn - self.dr_dev
+        k = self.kernel
+        mr = p if isinstance(p, torch.Tensor) else np.asarray(p, dtype=np.float64)
+        v = k.ws.lsrtm_misfit(mr, self.dr_dev, k._range())
+        k.born_applies += 1
+        if k.shard is not None:
+            v = k.shard.allreduce_value(v)
+        return v
 
     def residual_norm(self, p):
-        r = self._resid(p)
-        v = float((r.double() ** 2).sum().item())
-        if self.kernel.shard is not None:
-            v = self.kernel.shard.allreduce_value(v)
-        return float(np.sqrt(v))
+        """||L m_r - d_r||; one Born apply (seisopt/gradients.py:351-361)."""
+        return float(np.sqrt(2.0 * self._half_sq(p)))
 
     def value(self, p):
+        """seisopt/gradients.py:363-369."""
         self.counters.obj_evals += 1
-        r = self._resid(p)
-        v = 0.5 * float((r.double() ** 2).sum().item())
-        if self.kernel.shard is not None:
-            v = self.kernel.shard.allreduce_value(v)
-        return v
+        return float(self._half_sq(p))
 
     def value_and_grad(self, p):
         torch = _torch()

@@ -5,7 +5,9 @@ seisopt/optim/quasi_newton.py:16-208 and seisopt/optim/linesearch.py:29-70;
 the code is organised around direction-rule objects driven by one loop.
 
 Iterates, gradients and curvature pairs stay torch tensors on the problem's
-device; only scalars (inner products, objective values) reach the host.
+device; inner products and vector updates run in libseisgpu's fused vector
+kernels (``devvec``), and only scalars (inner products, objective values)
+reach the host.
 """
 
 from __future__ import annotations
@@ -15,6 +17,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import devvec
 from .anderson import OptimizeResult, OptimizerReport, _budget_allows, default_eta
 
 CURVATURE_SKIP_TOL = 1e-12  # seisopt/optim/quasi_newton.py:13
@@ -26,11 +29,16 @@ def _torch():
 
 
 def _ip(a, b):
-    return float(a.double().dot(b.double()).item())
+    return devvec.dot(a, b)
 
 
 def _len(a):
-    return float(a.double().norm().item())
+    return devvec.norm(a)
+
+
+def _lin(coefs, xs, y=None):
+    """y + sum_i coefs[i] xs[i] as a new vector (one device pass)."""
+    return devvec.axpy(coefs, xs, y)
 
 
 class LineSearchError(Exception):
@@ -59,7 +67,7 @@ def backtracking_line_search(value_fn, p, direction, grad_p, value_p, initial_st
     for n_try in range(1, max_backtracks + 1):
         if budget_ok is not None and not budget_ok():
             return LineSearchResult(0.0, value_p, n_try - 1, False)
-        trial_point = p + s * direction
+        trial_point = _lin([s], [direction], p)
         f = value_fn(trial_point)
         if np.isfinite(f) and f <= value_p + c1 * s * slope:
             ok = None if grad_fn is None else bool(
@@ -99,13 +107,13 @@ class LBFGSHistory:
         coeff = []
         for dp, dg, rho in reversed(self._q):
             a = rho * _ip(dp, q)
-            q.sub_(dg, alpha=a)
+            devvec.axpy([-a], [dg], q, out=q)
             coeff.append(a)
         if self._q:
             dp, dg, _ = self._q[-1]
-            q.mul_(_ip(dp, dg) / _ip(dg, dg))
+            devvec.scale(_ip(dp, dg) / _ip(dg, dg), q, out=q)
         for (dp, dg, rho), a in zip(self._q, reversed(coeff)):
-            q.add_(dp, alpha=a - rho * _ip(dg, q))
+            devvec.axpy([a - rho * _ip(dg, q)], [dp], q, out=q)
         return q
 
 
@@ -119,16 +127,16 @@ class _LBFGSRule:
         self.hist = LBFGSHistory(memory)
 
     def direction(self, g, eta0):
-        d = -self.hist.apply(g)
+        d = devvec.scale(-1.0, self.hist.apply(g))
         if _ip(d, g) >= 0.0:
             self.hist.clear()
-            d = -g
+            d = devvec.scale(-1.0, g)
         return d, (1.0 if self.hist._q else eta0)
 
     def accepted(self, p, g, p_new, g_new, d, fell_back):
         if fell_back:
             self.hist.clear()
-        self.hist.push(p_new - p, g_new - g)
+        self.hist.push(_lin([-1.0], [p], p_new), _lin([-1.0], [g], g_new))
 
 
 class _PRPlusRule:
@@ -142,19 +150,20 @@ class _PRPlusRule:
 
     def direction(self, g, eta0):
         if self.g_prev is None:
-            d = -g
+            d = devvec.scale(-1.0, g)
         else:
-            beta = max(0.0, _ip(g, g - self.g_prev) / _ip(self.g_prev, self.g_prev))
-            d = -g + beta * self.d_prev
+            beta = max(0.0, _ip(g, _lin([-1.0], [self.g_prev], g)) /
+                       _ip(self.g_prev, self.g_prev))
+            d = _lin([-1.0, beta], [g, self.d_prev])
             if _ip(d, g) >= 0.0:
-                d = -g
+                d = devvec.scale(-1.0, g)
         self.d_prev = d
         return d, (eta0 if self.s_prev is None else 2.0 * self.s_prev)
 
     def accepted(self, p, g, p_new, g_new, d, fell_back):
         self.g_prev, self.d_prev = g, d
         dl = _len(d)
-        self.s_prev = _len(p_new - p) / dl if dl else None
+        self.s_prev = _len(_lin([-1.0], [p], p_new)) / dl if dl else None
 
 
 def _drive(problem, p0, rule, budget, max_iters, grad_tol, c1, c2, max_backtracks, line_search):
@@ -204,8 +213,8 @@ def _drive(problem, p0, rule, budget, max_iters, grad_tol, c1, c2, max_backtrack
                 if ls.success:
                     step = ls.step
                 else:  # small steepest-descent step (quasi_newton.py:63-72)
-                    step, d, fell_back = eta0, -g, True
-            p_new = p + step * d
+                    step, d, fell_back = eta0, devvec.scale(-1.0, g), True
+            p_new = _lin([step], [d], p)
         report.append(iteration=k, objective=f, grad_norm=gnorm,
                       grad_evals=problem.counters.grad_evals,
                       obj_evals=problem.counters.obj_evals, step=step)

@@ -68,20 +68,24 @@ class ShotShard:
         return float(t.item())
 
     def allreduce_value_grad(self, value: float, grad) -> float:
-        """One collective for gradient (in place) and misfit."""
+        """Gradient summed in place over the ranks, misfit summed in fp64.
+
+        fp64 gradients carry the misfit in the same buffer (one collective,
+        exact).  fp32 gradients are reduced in their own dtype and the misfit
+        in a separate fp64 all-reduce, so the value handed to the optimizer's
+        Armijo test has the same precision as FwiObjective.value's."""
         import torch
         dist = self._dist()
         if dist is None:
             return float(value)
         flat = grad.reshape(-1)
-        n = flat.numel()
-        buf = torch.empty(n + 2, dtype=grad.dtype, device=grad.device)
-        buf[:n].copy_(flat)
-        # misfit as a (hi, lo) pair so an fp32 buffer still carries ~fp64 precision
-        hi = float(torch.tensor(float(value), dtype=grad.dtype).item())
-        buf[n] = hi
-        buf[n + 1] = float(value) - hi
-        dist.all_reduce(buf, group=self.group)
-        flat.copy_(buf[:n])
-        pair = buf[n:].double().cpu()
-        return float(pair[0].item() + pair[1].item())
+        if grad.dtype == torch.float64:
+            n = flat.numel()
+            buf = torch.empty(n + 1, dtype=grad.dtype, device=grad.device)
+            buf[:n].copy_(flat)
+            buf[n] = float(value)
+            dist.all_reduce(buf, group=self.group)
+            flat.copy_(buf[:n])
+            return float(buf[n].item())
+        dist.all_reduce(flat, group=self.group)
+        return self.allreduce_value(value)

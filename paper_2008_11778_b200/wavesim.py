@@ -188,7 +188,9 @@ class Propagator:
             "geometry")
         self.wavelet = np.ascontiguousarray(samples)
         _lib.check(self.lib.sg_set_wavelet(h, _lib.hptr_d(self.wavelet)), "wavelet")
-        self._lock = threading.Lock()
+        # serialises set_model + sweep pairs of callers sharing this handle
+        # (the module functions' cached propagators; ctypes releases the GIL)
+        self._lock = threading.RLock()
         self.model_token = None
 
     # -- plumbing -----------------------------------------------------------
@@ -313,6 +315,17 @@ class Propagator:
                                               1 if accumulate else 0), "lsrtm_gradient")
         return v.value, out
 
+    def lsrtm_misfit(self, m_r, d_r, shots=None):
+        """1/2 ||L m_r - d_r||^2 over the shots, reduced on the device."""
+        s0, cnt = self._range(shots)
+        mr = self.to_dev(m_r).reshape(self.grid.nz, self.grid.nx).contiguous()
+        dr = self.to_dev(d_r)
+        v = C.c_double()
+        self._stream()
+        _lib.check(self.lib.sg_lsrtm_misfit(self.h, s0, cnt, _lib.dptr(mr), _lib.dptr(dr),
+                                            C.byref(v)), "lsrtm_misfit")
+        return v.value
+
     def forward_history(self, shot):
         torch = _torch()
         g = torch.empty((self.nt, self.n_rec), device=self.device, dtype=self.tdtype)
@@ -349,6 +362,13 @@ class Propagator:
     def chains(self, count=None):
         """Concurrent shot chains a sweep over `count` shots runs as."""
         return int(self.lib.sg_chains(self.h, int(self.n_shots if count is None else count)))
+
+    def phase_times(self):
+        """Device ms of the last gradient's phases: forward sweep, residual +
+        injection, adjoint sweep (with imaging), image reduction."""
+        out = (C.c_float * 4)()
+        _lib.check(self.lib.sg_phase_times(self.h, out), "phase_times")
+        return dict(forward=out[0], residual=out[1], adjoint=out[2], reduce=out[3])
 
     def time_step_kernel(self, which, count=None, reps=50):
         ms = C.c_float()
@@ -392,15 +412,14 @@ def get_propagator(grid, geometry, wavelet, config=SimConfig(), dtype="float64",
     with _CACHE_LOCK:
         _CACHE[key] = prop
         while len(_CACHE) > _CACHE_MAX:
-            _, old = _CACHE.popitem(last=False)
-            old.close()
+            # dropped, not closed: a caller may still hold it (workspace=...);
+            # the handle is released when the last reference goes (__del__)
+            _CACHE.popitem(last=False)
     return prop
 
 
 def clear_cache():
     with _CACHE_LOCK:
-        for p in _CACHE.values():
-            p.close()
         _CACHE.clear()
 
 
@@ -440,16 +459,17 @@ def forward_solve(model, wavelet, geometry, source_index, config=SimConfig(), wo
     if not (0 <= source_index < geometry.n_sources):
         raise ValueError(f"source_index {source_index} out of range")
     prop = workspace or get_propagator(model.grid, geometry, wavelet, config, dtype)
-    prop.set_model(model.m)
-    if keep_history:
-        g, a = prop.forward_history(source_index)
-        hist = WavefieldHistory(accel=a.double().cpu().numpy(), pad=prop.pad, grid=model.grid,
-                                dt=geometry.dt)
-    else:
-        g = prop.synthetic((source_index, 1))[0]
-        hist = None
-    return ShotGather(source_index=source_index, samples=g.double().cpu().numpy(),
-                      dt=geometry.dt), hist
+    with prop._lock:  # model + sweep on one shared handle (see get_propagator)
+        prop.set_model(model.m)
+        if keep_history:
+            g, a = prop.forward_history(source_index)
+            hist = WavefieldHistory(accel=a.double().cpu().numpy(), pad=prop.pad,
+                                    grid=model.grid, dt=geometry.dt)
+        else:
+            g = prop.synthetic((source_index, 1))[0]
+            hist = None
+        g = g.double().cpu().numpy()
+    return ShotGather(source_index=source_index, samples=g, dt=geometry.dt), hist
 
 
 def adjoint_solve(model, adjoint_source, geometry, config=SimConfig(), workspace=None,
@@ -459,10 +479,10 @@ def adjoint_solve(model, adjoint_source, geometry, config=SimConfig(), workspace
         raise ValueError("adjoint source shape does not match geometry")
     wav = wavelet if wavelet is not None else np.zeros(geometry.nt)
     prop = workspace or get_propagator(model.grid, geometry, wav, config, dtype)
-    prop.set_model(model.m)
-    v = prop.adjoint_history(adjoint_source.samples)
-    return AdjointHistory(v=v.double().cpu().numpy(), pad=prop.pad, grid=model.grid,
-                          dt=geometry.dt)
+    with prop._lock:
+        prop.set_model(model.m)
+        v = prop.adjoint_history(adjoint_source.samples).double().cpu().numpy()
+    return AdjointHistory(v=v, pad=prop.pad, grid=model.grid, dt=geometry.dt)
 
 
 def born_solve(background, reflectivity, wavelet, geometry, source_index, config=SimConfig(),
@@ -471,7 +491,7 @@ def born_solve(background, reflectivity, wavelet, geometry, source_index, config
     if background.grid != reflectivity.grid:
         raise ValueError("background and reflectivity must share a grid")
     prop = workspace or get_propagator(background.grid, geometry, wavelet, config, dtype)
-    prop.set_model(background.m)
-    d = prop.born_forward(reflectivity.m_r, (source_index, 1))[0]
-    return ShotGather(source_index=source_index, samples=d.double().cpu().numpy(),
-                      dt=geometry.dt)
+    with prop._lock:
+        prop.set_model(background.m)
+        d = prop.born_forward(reflectivity.m_r, (source_index, 1))[0].double().cpu().numpy()
+    return ShotGather(source_index=source_index, samples=d, dt=geometry.dt)

@@ -84,19 +84,30 @@ def ref_types(case):
 
 
 class Recorder:
-    """Wraps an objective and records every model passed to value_and_grad."""
+    """Wraps an objective and records every model passed to value_and_grad
+    (and the value and gradient the reference returned for it)."""
 
     def __init__(self, inner):
         self.inner = inner
         self.counters = inner.counters
         self.models = []
+        self.values = []
+        self.grads = []
 
     def value(self, p):
         return self.inner.value(p)
 
     def value_and_grad(self, p):
         self.models.append(np.array(p, copy=True))
-        return self.inner.value_and_grad(p)
+        v, g = self.inner.value_and_grad(p)
+        self.values.append(v)
+        self.grads.append(np.array(g, copy=True))
+        return v, g
+
+
+def report_rows(res):
+    return np.array([[r.iteration, r.objective, r.grad_norm, r.grad_evals, r.obj_evals,
+                      r.step] for r in res.report.rows])
 
 
 def make_c1(order, with_aa):
@@ -114,9 +125,11 @@ def make_c1(order, with_aa):
         res = A.minimize_aa(obj, init.m.ravel(), memory=5, max_iters=20)
         rows = np.array([[r.iteration, r.objective, r.grad_norm, r.grad_evals, r.obj_evals,
                           r.step] for r in res.report.rows])
-        keep = [1, 2, 5, 10, 20]
+        keep = [0, 1, 2, 5, 10, 19, 20]
         out.update(aa_rows=rows, aa_eta=res.extras["eta"], aa_keep=np.array(keep),
                    aa_iterates=np.stack([obj.models[k] for k in keep]),
+                   aa_values=np.array([obj.values[k] for k in keep]),
+                   aa_grads=np.stack([obj.grads[k] for k in keep]),
                    aa_final=res.p)
     np.savez_compressed(os.path.join(HERE, f"c1_o{order}.npz"), **out)
 
@@ -178,6 +191,108 @@ def make_small(order, damp_top):
                             eta=res.extras["eta"], iterates=np.stack(obj.models),
                             final=res.p, lambdas=np.array(res.extras["lambdas"]),
                             sd_final=sd.p, **versions())
+
+
+def small_problem():
+    """small_o8_top inputs through the reference: model, true model, observed."""
+    use_order(8)
+    grid, model, geom, wav, cfg = small_setup(8, True)
+    c_true = model.velocity.copy()
+    c_true[18:24, 25:35] *= 1.06
+    true = VelocityModel.from_velocity(grid, c_true)
+    obs = G.fwi_synthetic(true, wav, geom, cfg)
+    return grid, model, geom, wav, cfg, obs
+
+
+def make_solves():
+    """Public single-shot solves (wavesim.py:354-430) on the small 8th-order
+    case: forward_solve with history, born_solve (from the history and
+    without), adjoint_solve.  Histories are stored as per-step norms plus a
+    few whole planes (the full (nt, nzp, nxp) arrays are 10 MB each)."""
+    grid, model, geom, wav, cfg, obs = small_problem()
+    rng = np.random.default_rng(3)
+    m_r = rng.standard_normal(grid.shape) * 1e-8
+    refl = ReflectivityModel(grid, m_r)
+    gat, hist = W.forward_solve(model, wav, geom, 1, cfg)
+    gat_nohist, none = W.forward_solve(model, wav, geom, 0, cfg, keep_history=False)
+    born_h = W.born_solve(model, refl, wav, geom, 1, cfg, background_history=hist)
+    born0 = W.born_solve(model, refl, wav, geom, 0, cfg)
+    ybar = W.ShotGather(0, rng.standard_normal((geom.nt, geom.n_receivers)), geom.dt)
+    adj = W.adjoint_solve(model, ybar, geom, cfg)
+    planes = np.array([10, 77, 150, 299])
+    np.savez_compressed(
+        os.path.join(HERE, "solves.npz"), m_r=m_r, gather1=gat.samples,
+        gather0=gat_nohist.samples, hist_none=none is None,
+        accel_norms=np.linalg.norm(hist.accel.reshape(geom.nt, -1), axis=1),
+        accel_planes=hist.accel[planes], planes=planes,
+        accel_phys=hist.accel_physical(150), born1=born_h.samples, born0=born0.samples,
+        ybar=ybar.samples, v_norms=np.linalg.norm(adj.v.reshape(geom.nt, -1), axis=1),
+        v_planes=adj.v[planes], **versions())
+
+
+def make_lsrtm_objective():
+    """LsrtmObjective (gradients.py:339-378) on the small case: value,
+    value_and_grad, residual_norm, and the counters / kernel applies they
+    leave (born_applies, adjoint_applies, grad_equivalents)."""
+    grid, model, geom, wav, cfg, obs = small_problem()
+    rng = np.random.default_rng(7)
+    kern = G.BornKernel(model, wav, geom, cfg)
+    m_true = rng.standard_normal(grid.shape) * 1e-8
+    d_r = kern.forward(m_true)
+    obj = G.LsrtmObjective(kern, d_r)
+    p = (0.3 * m_true + 1e-9 * rng.standard_normal(grid.shape)).ravel()
+    v = obj.value(p)
+    vg, g = obj.value_and_grad(p)
+    rn = obj.residual_norm(p)
+    v0 = obj.value(np.zeros_like(p))
+    np.savez_compressed(
+        os.path.join(HERE, "lsrtm_objective.npz"), m_true=m_true, p=p, value=v,
+        vg_value=vg, grad=g, residual_norm=rn, value0=v0,
+        d_r=np.stack([d.samples for d in d_r]),
+        counters=np.array([obj.counters.grad_evals, obj.counters.obj_evals]),
+        applies=np.array([kern.born_applies, kern.adjoint_applies, kern.grad_equivalents]),
+        **versions())
+    # restarted GMRES on the normal equations (krylov.py:224-258), both starts
+    from seisopt import krylov as K
+    out = {}
+    for tag, restart, iters, zero in (("rtm", 3, 9, False), ("zero", 5, 15, True)):
+        kk = G.BornKernel(model, wav, geom, cfg)
+        x, res = K.lsrtm_gmres(model, d_r, wav, geom, cfg, restart=restart, iterations=iters,
+                               zero_start=zero, kernel=kk)
+        out[f"{tag}_x"] = x
+        out[f"{tag}_hist"] = np.array([[h.outer_iter, h.inner_iter, h.residual_norm,
+                                        h.grad_equivalents] for h in res.history])
+        out[f"{tag}_converged"] = res.converged
+        out[f"{tag}_applies"] = np.array([kk.born_applies, kk.adjoint_applies])
+    np.savez_compressed(os.path.join(HERE, "lsrtm_gmres.npz"), d_r=np.stack([d.samples for d in d_r]),
+                        **out, **versions())
+
+
+def make_quasi_newton():
+    """minimize_lbfgs / minimize_ncg (optim/quasi_newton.py:123-208) on the
+    small FWI problem, and the gradient-equivalent budget veto
+    (optim/anderson.py:229-232) of minimize_aa / minimize_sd / minimize_lbfgs."""
+    from seisopt.optim import quasi_newton as QN
+    grid, model, geom, wav, cfg, obs = small_problem()
+    out = {}
+    res = QN.minimize_lbfgs(G.FwiObjective(grid, obs, wav, geom, cfg), model.m.ravel(),
+                            memory=3, max_iters=4)
+    out.update(lbfgs_rows=report_rows(res), lbfgs_final=res.p, lbfgs_eta=res.extras["eta"])
+    res = QN.minimize_ncg(G.FwiObjective(grid, obs, wav, geom, cfg), model.m.ravel(),
+                          max_iters=3)
+    out.update(ncg_rows=report_rows(res), ncg_final=res.p)
+    # budget veto: stops on grad_equivalents + cost > budget
+    for tag, fn in (("aa", lambda o: A.minimize_aa(o, model.m.ravel(), memory=3, budget=5.5)),
+                    ("sd", lambda o: A.minimize_sd(o, model.m.ravel(), budget=3.0,
+                                                   line_search=True)),
+                    ("lbfgs", lambda o: QN.minimize_lbfgs(o, model.m.ravel(), memory=3,
+                                                          budget=4.5))):
+        o = G.FwiObjective(grid, obs, wav, geom, cfg)
+        r = fn(o)
+        out[f"budget_{tag}_rows"] = report_rows(r)
+        out[f"budget_{tag}_final"] = r.p
+        out[f"budget_{tag}_counters"] = np.array([o.counters.grad_evals, o.counters.obj_evals])
+    np.savez_compressed(os.path.join(HERE, "quasi_newton.npz"), **out, **versions())
 
 
 def make_aa_window():
@@ -296,6 +411,36 @@ def make_aa_run():
     np.savez_compressed(os.path.join(HERE, "sd_linesearch.npz"), rows=rows, final=res.p,
                         eta=res.extras["eta"], big_rows=big_rows, big_final=big.p,
                         **versions())
+
+
+def make_c3(threads=6):
+    """The benched workload itself (BASELINE configs[2], C3): the full 30-shot,
+    nt 4000 FWI gradient of the reference (`gradients.py:118-155`) at the
+    smoothed initial model, observed data synthesised by the reference from
+    the seeded layered-fault true model (`gradients.py:98-115`), 8th order.
+    The 30 x 4000 x 601 observed gathers (577 MB) are not stored: the fixture
+    keeps per-shot norms and a few full traces of them (and of the synthetic
+    at the initial model) so a GPU test can pin its own synthesis first."""
+    use_order(8)
+    case = synthetic.layered_case("c3")
+    grid, geom, wav, cfg = ref_types(case)
+    true = VelocityModel(grid, case["true"].m)
+    init = VelocityModel(grid, case["init"].m)
+    obs = G.fwi_synthetic(true, wav, geom, cfg, threads=threads)
+    syn = G.fwi_synthetic(init, wav, geom, cfg, threads=threads)
+    ev = G.fwi_gradient(init, obs, wav, geom, cfg, threads=threads)
+    shot_misfit = np.array([G.misfit_l2([s], [o]) for s, o in zip(syn, obs)])
+    trace_shots = np.array([0, 11, 29])
+    trace_recs = np.array([0, 300, 600])
+    np.savez_compressed(
+        os.path.join(HERE, "c3_full.npz"),
+        m_init=init.m, m_true_sum=float(np.sum(true.m)), value=ev.value, grad=ev.gradient,
+        obs_norm=np.array([np.linalg.norm(o.samples) for o in obs]),
+        syn_norm=np.array([np.linalg.norm(s.samples) for s in syn]),
+        shot_misfit=shot_misfit, trace_shots=trace_shots, trace_recs=trace_recs,
+        obs_traces=np.stack([obs[s].samples[:, trace_recs] for s in trace_shots]),
+        syn_traces=np.stack([syn[s].samples[:, trace_recs] for s in trace_shots]),
+        order=8, **versions())
 
 
 if __name__ == "__main__":

@@ -46,7 +46,7 @@ def test_desc_layout_matches_header():
 def test_version_and_error_string(lib):
     from paper_2008_11778_b200 import _lib
     L = _lib.load()
-    assert L.sg_version() == 1
+    assert L.sg_version() == 2
     # argument validation needs no device: a null descriptor is rejected
     h = ctypes.c_void_p()
     rc = L.sg_create(None, ctypes.byref(h))

@@ -575,6 +575,12 @@ def test_c3_fp32_aa_misfit_curve_vs_fp64():
     assert np.array_equal(mine[:, 1], ref[:, 1])
 
 
+def _need_experimental():
+    from paper_2008_11778_b200 import _lib
+    if not _lib.experimental_kernels():
+        pytest.skip("opt-in kernels not compiled (build with defines=('SG_EXPERIMENTAL=1',))")
+
+
 @pytest.mark.parametrize("order", [2, 8])
 @pytest.mark.parametrize("recon", ["full", "checkpoint"])
 def test_two_step_kernel_matches_one_step(order, recon):
@@ -588,6 +594,7 @@ def test_two_step_kernel_matches_one_step(order, recon):
     either adjoint form -- residual cancellation in the forward data,
     tools/adj3_err.py, profiles/r01e_adj3_err.log -- so it is compared
     between the kernels only.)"""
+    _need_experimental()
     _, wavesim = _api()
     case = small_case(order, True)
     g = case["gold"]
@@ -728,6 +735,7 @@ def test_resident_sweeps_match_one_step():
     of per-group image planes; the resident adjoint keeps the V/w increment
     form, the one-step kernel runs the three-level recurrence), and the fp32
     gradient within the north-star tolerance of the fp64 reference golden."""
+    _need_experimental()
     _, wavesim = _api()
     case = c1(8)
     g = case["gold"]

@@ -168,3 +168,85 @@ def test_sd_armijo_trajectory():
     assert np.array_equal(rows[:, [0, 3, 4]], g["big_rows"][:, [0, 3, 4]])
     assert np.allclose(rows[:, [1, 2, 5]], g["big_rows"][:, [1, 2, 5]], rtol=1e-12)
     assert rel(big["p"], g["big_final"]) <= 1e-12
+
+
+# ---------------------------------------------------------------------------
+# round-2 fixtures: the oracle must reproduce them as well
+# ---------------------------------------------------------------------------
+
+
+def test_c3_full_fixture_one_shot():
+    """Shot 11 of the benched C3 workload (201 x 601, nt 4000, 8th order):
+    the oracle's synthesis of the true and initial models reproduces the
+    reference's per-shot norms, traces and misfit (c3_full.npz)."""
+    from paper_2008_11778_b200 import synthetic
+    g = golden("c3_full")
+    case = synthetic.layered_case("c3")
+    assert rel(case["init"].m, g["m_init"]) <= 1e-14
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    s = 11
+    ts = list(g["trace_shots"])
+    k = ts.index(s)
+    out = []
+    for m in (case["true"].m, case["init"].m):
+        st = oracle_setup(m, grid, geom, cfg)
+        tr, _ = oracle.forward_sweep(st, geom.nt, amp=wav.samples, shot=s, keep=False)
+        out.append(tr)
+    obs, syn = out
+    assert abs(np.linalg.norm(obs) - g["obs_norm"][s]) <= TOL * g["obs_norm"][s]
+    assert abs(np.linalg.norm(syn) - g["syn_norm"][s]) <= TOL * g["syn_norm"][s]
+    assert rel(obs[:, g["trace_recs"]], g["obs_traces"][k]) <= TOL
+    assert rel(syn[:, g["trace_recs"]], g["syn_traces"][k]) <= TOL
+    mis = oracle.misfit_l2([syn], [obs], geom.dt)
+    assert abs(mis - g["shot_misfit"][s]) <= 1e-12 * g["shot_misfit"][s]
+
+
+def test_solves_fixture():
+    """forward_solve / born_solve / adjoint_solve (wavesim.py:354-430)."""
+    g = golden("solves")
+    case = small_case(8, True)
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    st = oracle_setup(case["gold"]["m"], grid, geom, cfg)
+    tr, hist = oracle.forward_sweep(st, geom.nt, amp=wav.samples, shot=1, keep=True)
+    assert rel(tr, g["gather1"]) <= TOL
+    assert rel(np.linalg.norm(hist.reshape(geom.nt, -1), axis=1), g["accel_norms"]) <= TOL
+    assert rel(hist[g["planes"]], g["accel_planes"]) <= TOL
+    scale = -oracle.extend_to_pad(g["m_r"], st.pads)
+    born1, _ = oracle.forward_sweep(st, geom.nt, grid_src=hist, grid_scale=scale, keep=False)
+    assert rel(born1, g["born1"]) <= TOL
+    _, vh = oracle.adjoint_sweep(st, g["ybar"], keep_v=True)
+    assert rel(np.linalg.norm(vh.reshape(geom.nt, -1), axis=1), g["v_norms"]) <= TOL
+    assert rel(vh[g["planes"]], g["v_planes"]) <= TOL
+
+
+def test_lsrtm_objective_fixture():
+    """LsrtmObjective value / gradient / residual norm (gradients.py:339-378)."""
+    g = golden("lsrtm_objective")
+    case = small_case(8, True)
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    st = oracle_setup(case["gold"]["m"], grid, geom, cfg)
+    born = oracle.BornOracle(st, wav.samples, geom.nt)
+    assert rel(np.stack(born.forward(g["m_true"])), g["d_r"]) <= TOL
+    obj = oracle.LsrtmOracleObjective(born, list(g["d_r"]))
+    v = obj.value(g["p"])
+    vg, grad = obj.value_and_grad(g["p"])
+    assert abs(v - float(g["value"])) <= TOL * float(g["value"])
+    assert abs(vg - float(g["vg_value"])) <= TOL * float(g["vg_value"])
+    assert rel(grad, g["grad"]) <= TOL
+
+
+def test_budget_fixture_minimize_aa():
+    """minimize_aa's gradient-equivalent budget veto (anderson.py:229-232)."""
+    g = golden("quasi_newton")
+    case = small_case(8, True)
+    geom, grid, cfg, wav = case["geometry"], case["grid"], case["config"], case["wavelet"]
+    obs = list(case["gold"]["obs"])
+    obj = oracle.FwiOracleObjective(lambda m: oracle_setup(m, grid, geom, cfg), obs,
+                                    wav.samples, geom.nt, (grid.nz, grid.nx))
+    res = oracle.minimize_aa(obj, case["gold"]["m"].ravel(), memory=3, budget=5.5)
+    rows = np.asarray(res["rows"], dtype=np.float64)
+    assert rel(res["p"], g["budget_aa_final"]) <= 1e-12
+    ref = g["budget_aa_rows"]
+    assert rows.shape == ref.shape
+    assert np.array_equal(rows[:, [0, 3, 4]], ref[:, [0, 3, 4]])
+    assert np.allclose(rows[:, 1], ref[:, 1], rtol=1e-12)
