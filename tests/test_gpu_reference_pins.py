@@ -199,8 +199,10 @@ def test_lsrtm_objective_matches_reference(cache):
     assert abs(rn - float(g["residual_norm"])) <= F64 * float(g["residual_norm"])
     assert abs(v0 - float(g["value0"])) <= F64 * float(g["value0"])
     assert [obj.counters.grad_evals, obj.counters.obj_evals] == list(g["counters"])
-    assert [kern.born_applies, kern.adjoint_applies] == list(g["applies"][:2])
-    assert kern.grad_equivalents == float(g["applies"][2])
+    # the reference's kernel also made d_r (one more Born apply, make_golden.py)
+    ref_born, ref_adj, ref_ge = (float(x) for x in g["applies"])
+    assert [kern.born_applies, kern.adjoint_applies] == [ref_born - 1, ref_adj]
+    assert kern.grad_equivalents == ref_ge - 0.5
 
 
 @pytest.mark.parametrize("tag,restart,iters,zero", [("rtm", 3, 9, False), ("zero", 5, 15, True)])

@@ -19,11 +19,14 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--dtype", default="float32")
     ap.add_argument("--recon", default="full")
+    ap.add_argument("--shots", type=int, default=None)
+    ap.add_argument("--nt", type=int, default=None)
     a = ap.parse_args()
     import torch
     from paper_2008_11778_b200 import synthetic
     from paper_2008_11778_b200.wavesim import Propagator
-    case = synthetic.layered_case(a.config) if a.config != "c1" else synthetic.c1_case()
+    case = (synthetic.layered_case(a.config, n_shots=a.shots, nt=a.nt) if a.config != "c1"
+            else synthetic.c1_case())
     prop = Propagator(case["grid"], case["geometry"], case["wavelet"], case["config"],
                       dtype=a.dtype, recon=a.recon, use_graphs=False)
     prop.set_model(case["init"].m)
