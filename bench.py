@@ -125,6 +125,13 @@ def clock_sampler(index):
         return ClockSampler(index)
 
 
+def l2_cap_gbs(clocks):
+    """L2 (LTS) throughput cap: ~6300 B/cycle full chip (measured,
+    /opt/skills/guides/B300_MICROARCH.md) at the SM clock this run sampled."""
+    mhz = (clocks or {}).get("sm_mhz")
+    return 6300.0 * mhz * 1e6 / 1e9 if mhz else None
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as fh:
@@ -471,14 +478,20 @@ def c5_kernel_record(dev, peak, peak_src, reps=400, shots=8, nt=400):
         tr = json.load(open(tpath)).get("c5", {})
     out = {"grid": "1041x3041 padded (C5)", "shots_per_launch": shots, "reps": reps,
            "peak": peak, "peak_source": peak_src}
-    for name, ms, alg_b in (("forward_band_step", ms_fwd, 4 * es),
-                            ("reverse_adjoint_step", ms_adj, 8 * es + 3 * es)):
+    # kmin: the bytes the kernel as designed must move per shot-cell -- forward
+    # u, inc in and out (16 B); fused reverse + adjoint with both three-level
+    # recurrences: V_n, V_{n+1}, u_n, u_{n+1} in, V_{n-1}, u_{n-1} out (24 B;
+    # the image accumulates per CTA group, the band store is <6 % of cells)
+    for name, ms, alg_b, kmin_b in (("forward_band_step", ms_fwd, 4 * es, 4 * es),
+                                    ("reverse_adjoint_step", ms_adj, 8 * es + 3 * es, 6 * es)):
         alg = shots * C * alg_b
         dram = tr.get(name)
         dram_step = dram * shots if (dram is not None and tr.get("per_shot")) else dram
         out[name] = {
             "ms_per_step": ms, "alg_bytes_per_shot_cell": alg_b,
             "alg_gbs": alg / (ms / 1e3) / 1e9, "alg_frac": alg / (ms / 1e3) / 1e9 / peak,
+            "kernel_min_bytes_per_shot_cell": kmin_b,
+            "kernel_min_frac": shots * C * kmin_b / (ms / 1e3) / 1e9 / peak,
             "dram_bytes_per_step": dram_step,
             "dram_gbs": (dram_step / (ms / 1e3) / 1e9) if dram_step else None,
             "dram_frac": (dram_step / (ms / 1e3) / 1e9 / peak) if dram_step else None,
@@ -617,15 +630,29 @@ def run_ours(args):
             traffic_tab = json.load(open(tpath)).get(args.config, {})
         except Exception:
             traffic_tab = {}
+    clocks = clk.summary()
+    l2_cap = l2_cap_gbs(clocks)
     for name, msk, byt, ph, iso_ms in ((names[0], ms_fwd, bytes_fwd, phases["forward"], iso_fwd),
                                        (names[1], ms_adj, bytes_adj, phases["adjoint"], iso_adj)):
         tr = traffic_tab.get(name)
-        if tr is not None and traffic_tab.get("per_shot"):
-            tr *= launch_shots
+        lts = (traffic_tab.get("lts") or {}).get(name)
+        if traffic_tab.get("per_shot"):
+            tr = tr * launch_shots if tr is not None else None
+            lts = lts * launch_shots if lts is not None else None
+        elif args.config == "c3" and launch_shots != 30:
+            # the committed C3 capture is of 30-shot steps
+            tr = tr * launch_shots / 30.0 if tr is not None else None
+            lts = lts * launch_shots / 30.0 if lts is not None else None
         kern[name] = {"ms_per_step": msk, "share": ph / total_ph if total_ph else None,
                       "bytes_per_step": byt, "achieved": byt / (msk / 1e3) / 1e9,
                       "frac": byt / (msk / 1e3) / 1e9 / peak, "traffic": tr,
                       "traffic_gbs": (tr / (msk / 1e3) / 1e9) if tr else None,
+                      # L2 tag-stage bytes (ncu lts__t_bytes.sum, steady state) over
+                      # the live step time, against the measured LTS cap of
+                      # ~6300 B/cycle at the SM clock sampled in this run
+                      "l2_bytes_per_step": lts,
+                      "l2_gbs": (lts / (msk / 1e3) / 1e9) if lts else None,
+                      "l2_frac": (lts / (msk / 1e3) / 1e9 / l2_cap) if (lts and l2_cap) else None,
                       "isolated_ms_per_step": iso_ms}
     dom = max(names, key=lambda n: kern[n]["share"] or 0.0)
     dk = kern[dom]
@@ -680,13 +707,16 @@ def run_ours(args):
                          # actually moved (C3 fields stay in L2, so < achieved)
                          "traffic_gbs": dk["traffic_gbs"],
                          "traffic_frac": (dk["traffic_gbs"] / peak) if dk["traffic_gbs"] else None,
+                         "l2": {"gbs": dk["l2_gbs"], "cap_gbs": l2_cap, "frac": dk["l2_frac"],
+                                "cap_source": "6300 B/cycle (B300_MICROARCH.md LTS cap) x "
+                                              "sampled SM clock"},
                          "shots_per_step": launch_shots,
                          "chains": prop.chains(launch_shots),
                          "bytes_per_step": dk["bytes_per_step"], "ms_per_step": dk["ms_per_step"],
                          "share": dk["share"], "timing": "gradient phase events / steps",
                          "kernels": kern},
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "cpu_baseline": cpu,
         }
         if c5 is not None:

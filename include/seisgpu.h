@@ -217,6 +217,16 @@ int sg_phase_times(sg_handle* h, float* ms_out);
 /* Number of kernel launches this handle (or AA window) has issued. */
 int64_t sg_launch_count(void);
 
+/* The library's own memcheck.  With SG_REDZONE=1 in the environment when the
+ * library is loaded, every device allocation of a handle or AA window carries
+ * 64 KB guard zones of 0xFF bytes (NaN in fp32 and fp64) on both sides: an
+ * out-of-bounds read poisons the results, an out-of-bounds write is counted
+ * here.  bad_bytes = guard bytes found modified (allocations already freed
+ * plus all live ones), allocations = guarded allocations made so far (0: the
+ * mode is off).  poke != 0 first overwrites one guard byte of a live
+ * allocation (self-test of the detection).  No reference counterpart. */
+int sg_redzone_check(int64_t* bad_bytes, int64_t* allocations, int32_t poke);
+
 /* ---- Anderson acceleration window on the device -------------------------
  * Replaces AAWindow / SlidingQR / aa_weights / aa_step
  * (seisopt/optim/anderson.py:55-148, seisopt/optim/qr.py:22-104) by a

@@ -86,6 +86,7 @@ SIGNATURES = {
     "sg_time_step_kernel": (C.c_int, [_P, _I32, _I32, _I32, C.POINTER(C.c_float)]),
     "sg_phase_times": (C.c_int, [_P, C.POINTER(C.c_float)]),
     "sg_launch_count": (C.c_int64, []),
+    "sg_redzone_check": (C.c_int, [C.POINTER(C.c_int64), C.POINTER(C.c_int64), _I32]),
     "sg_aa_create": (C.c_int, [_I64, _I32, _I32, _I32, C.POINTER(_P)]),
     "sg_aa_destroy": (C.c_int, [_P]),
     "sg_aa_set_stream": (C.c_int, [_P, _P]),
@@ -127,6 +128,14 @@ def load(path: str | None = None):
             fn.argtypes = args
         _lib = lib
         return lib
+
+
+def redzone_check(poke=False):
+    """(corrupted guard bytes, guarded allocations) of the SG_REDZONE=1 mode
+    (include/seisgpu.h sg_redzone_check); allocations == 0: the mode is off."""
+    bad, n = C.c_int64(), C.c_int64()
+    check(load().sg_redzone_check(C.byref(bad), C.byref(n), 1 if poke else 0), "redzone_check")
+    return bad.value, n.value
 
 
 def last_error() -> str:

@@ -666,7 +666,7 @@ int device_qr(sg_aa* a) {
   const int k = a->ncols;
   if (!a->Qd) {
     const size_t bytes = (size_t)(a->memory + 1) * a->ld * sizeof(double);
-    cudaError_t e = cudaMalloc((void**)&a->Qd, bytes);
+    cudaError_t e = rz_malloc((void**)&a->Qd, bytes);
     if (e != cudaSuccess) {
       cudaGetLastError();
       a->Qd = nullptr;
@@ -952,12 +952,12 @@ int sg_aa_create(int64_t n, int32_t memory, int32_t dtype, int32_t device, sg_aa
   a->ld = (n + 63) / 64 * 64;
   const size_t vb = (size_t)a->ld * dtype;
   const int slots = std::max(memory, 1);
-  cudaError_t e = cudaMalloc(&a->DF, vb * slots);
-  if (e == cudaSuccess) e = cudaMalloc(&a->DG, vb * slots);
-  if (e == cudaSuccess) e = cudaMalloc(&a->fk, vb);
-  if (e == cudaSuccess) e = cudaMalloc(&a->gk, vb);
-  if (e == cudaSuccess) e = cudaMalloc((void**)&a->part, sizeof(double) * kBlocks * (2 * kMaxMem + 3));
-  if (e == cudaSuccess) e = cudaMalloc((void**)&a->out, sizeof(double) * (2 * kMaxMem + 8));
+  cudaError_t e = rz_malloc(&a->DF, vb * slots);
+  if (e == cudaSuccess) e = rz_malloc(&a->DG, vb * slots);
+  if (e == cudaSuccess) e = rz_malloc(&a->fk, vb);
+  if (e == cudaSuccess) e = rz_malloc(&a->gk, vb);
+  if (e == cudaSuccess) e = rz_malloc((void**)&a->part, sizeof(double) * kBlocks * (2 * kMaxMem + 3));
+  if (e == cudaSuccess) e = rz_malloc((void**)&a->out, sizeof(double) * (2 * kMaxMem + 8));
   if (e != cudaSuccess) {
     sg_aa_destroy(a);
     cudaGetLastError();
@@ -973,7 +973,7 @@ int sg_aa_destroy(sg_aa* a) {
   if (!a) return SG_OK;
   cudaSetDevice(a->device);
   for (void* p : {a->DF, a->DG, a->fk, a->gk, (void*)a->part, (void*)a->out, (void*)a->Qd})
-    if (p) cudaFree(p);
+    if (p) rz_free(p);
   delete a;
   return SG_OK;
 }

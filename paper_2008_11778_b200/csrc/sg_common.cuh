@@ -44,6 +44,15 @@ struct Trace {
 
 inline void count_launch(int64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// Device allocations of the library.  With SG_REDZONE=1 in the environment
+// every allocation carries a 64 KB guard zone of 0xFF bytes (NaN as fp32 and
+// fp64) on both sides: an out-of-bounds read poisons the result with NaN, an
+// out-of-bounds write is found by rz_check / at free time (sg_redzone_check).
+// The library's own memcheck: compute-sanitizer is not available on the GPU
+// pool this was built on.  (sg_prop.cu defines these.)
+cudaError_t rz_malloc(void** p, size_t bytes);
+void rz_free(void* p);
+
 // deterministic block reduction of a double (blockDim.x multiple of 32, <= 1024)
 __device__ __forceinline__ double block_sum(double v) {
   __shared__ double red[32];

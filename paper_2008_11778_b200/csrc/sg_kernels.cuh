@@ -82,6 +82,32 @@ constexpr int kHalo = 4;
 #ifndef SG_EARLY_TMA
 #define SG_EARLY_TMA 1
 #endif
+// fp32 forward with exact global constants (default): stencil weights as
+// ratios to c_1 (r_2 = -1/8 exact, r_3 / r_4 split hi + lo), c_1/h^2 and dt^2
+// split hi + lo, sponge factor as 1 - e.  The fp32 rounding of these global
+// constants is a coherent velocity / time-step bias (phase error growing with
+// the step count); removing it cuts the fp32 gradient error 4-5x
+// (tools/fp32_scheme.py: C1 iterate 0 3.9e-5 -> 9.1e-6, iterate 19 1.07e-3 ->
+// 2.2e-4).  0 = the round-1 arithmetic (weights c_k/h^2, dt^2, d rounded).
+// Interior tiles (no sponge cell: d = 1, e = 0 for every cell of the CTA) run
+// the updates without the damping operations; bitwise the damped formulas at
+// d = 1.
+// Not in the fused reverse + adjoint kernel (its third code path spills at the
+// 128-register cap: C5 step 117 -> 133 us) nor, by default, in the lock-step
+// Born kernel.
+#ifndef SG_INNER
+#define SG_INNER 1
+#endif
+#ifndef SG_INNER_LOCK
+#define SG_INNER_LOCK 0
+#endif
+#ifndef SG_GC
+#if defined(SG_EXPERIMENTAL) && SG_EXPERIMENTAL
+#define SG_GC 0  // the opt-in two-step / resident kernels keep the round-1 arithmetic
+#else
+#define SG_GC 1
+#endif
+#endif
 // Image accumulators: one set, read after the PDL wait (default), or two
 // launch-parity sets prefetched before it (SG_IMG_PARITY=1).  One set halves
 // the adjoint's image footprint in L2 and measured faster: C3 gradient
@@ -112,6 +138,18 @@ struct StepArgs {
   int g0;                 // first image group plane of this launch
   T dt2;
   T cz[5], cx[5];         // stencil weights k = 1..R
+  // exact-constant forward (SG_GC, fp32): r_k = c_k / c_1 as hi + lo; the
+  // z scale K = c_1/dz^2 is folded into the per-cell model plane (inv_m holds
+  // K/m: per-cell rounding is incoherent and harmless), the source weights
+  // and the Born scale (both / K); rho = (c_1/dx^2) / K as hi + lo (1 when
+  // dx == dz: iso); dt^2 as hi + lo; sponge as e = 1 - d
+  T rh[5], rl[5];
+  T rhoh, rhol;
+  int iso;
+  T dt2l;                 // dt^2 - (T)dt^2
+  T cdt2;                 // adjoint coefficient scale: dt^2 / K (dt^2 without SG_GC)
+  const T* ez;            // 1 - pz (rows), rounded from fp64
+  const T* ex;            // 1 - px (cols)
   int hist_on;            // FWD: store history; ADJ: image against history
   int hist_steps, hist_slot;  // history plane of shot b at this step: b*hist_steps + slot
   T* hist;                // history base (plain stores of the forward)
@@ -494,6 +532,10 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
   constexpr bool LOAD_HIST = ADJ && HIST && !RB;
   constexpr bool IMG = LOAD_HIST || RB;  // adjoint image accumulation
   constexpr bool SRC = !ADJ || RB;       // forward acceleration with point source
+  // exact global constants in the fp32 forward recursion (SG_GC); GCD: the
+  // forward's dd[] holds -e = d - 1 instead of d
+  constexpr bool GC = SG_GC && sizeof(T) == 4 && SRC;
+  constexpr bool GCD = GC && !ADJ;
 
   // source taps of the group's shots, staged once (static data, PDL-safe)
   __shared__ int s_src[8 * 8];
@@ -553,11 +595,16 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
   const bool tile_band = (BSAVE || RB) && (i0 < a.bT || i0 + kTH > a.nzp - a.bB ||
                                            j0 < a.bL || j0 + kBX > a.nxp - a.bR);
 
+  // no sponge cell in this tile (CTA-uniform): d = 1 everywhere in it
+  const bool tile_inner = i0 >= a.bT && i0 + kTH <= a.nzp - a.bB && j0 >= a.bL &&
+                          j0 + kBX <= a.nxp - a.bR;
+
   // per-cell model data, reused for every shot of the group; the image
   // accumulator starts from the stored image (prefetched, lands during shot 0)
   P im[kNY], dd[kNY];
   T img[2 * kNY];
-  const T pxj0 = a.px[j], pxj1 = a.px[j + 1];  // zero beyond nxp (profile tail)
+  // zero beyond nxp (profile tail)
+  const T pxj0 = GCD ? a.ex[j] : a.px[j], pxj1 = GCD ? a.ex[j + 1] : a.px[j + 1];
   // Prologue (may overlap the previous step under PDL): model data and, with
   // SG_IMG_PARITY, the image accumulator of this launch's parity, last written
   // two launches ago (complete: the previous grid signalled its dependents
@@ -568,8 +615,15 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
   for (int q = 0; q < kNY; ++q) {
     if (q < nq) {
       im[q] = ldg2(a.inv_m + o0 + q * ldx);
-      const T pz = a.pz[ib + q];
-      dd[q] = P::make(pz * pxj0, pz * pxj1);
+      if constexpr (GCD) {
+        // -e = -(ez + ex - ez ex): 0 in the interior, d - 1 in the sponge
+        const T ez = a.ez[ib + q];
+        dd[q] = P::make(__fmaf_rn((float)ez, (float)pxj0, -((float)ez + (float)pxj0)),
+                        __fmaf_rn((float)ez, (float)pxj1, -((float)ez + (float)pxj1)));
+      } else {
+        const T pz = a.pz[ib + q];
+        dd[q] = P::make(pz * pxj0, pz * pxj1);
+      }
 #if SG_IMG_PARITY
       img[2 * q] = IMG ? ig[q * ldx] : T(0);
       img[2 * q + 1] = (IMG && vj1) ? ig[q * ldx + 1] : T(0);
@@ -582,6 +636,8 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
     }
   }
   const P dt2p = P::make(a.dt2, a.dt2);
+  const P dt2lp = P::make(a.dt2l, a.dt2l);
+  const P cdt2p = P::make(a.cdt2, a.cdt2);
   // everything below reads or writes fields/states of the previous step
   // (thread 0 already waited and put the first stages in flight, SG_EARLY_TMA)
   pdl_wait();
@@ -648,7 +704,9 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
       // sum_k c_k ((u_{-k} - u) + (u_{+k} - u)); vertical neighbours from the
       // register window, horizontal ones from 8-byte aligned shared loads
       // (odd offsets re-paired from their aligned neighbours)
-      auto lap2 = [&](const P* w, const T* s, int q) -> P {
+      // second-difference sums t_k = (u_{-k} - u) + (u_{+k} - u) of the pair,
+      // vertical (tz) and horizontal (tx), k = 1..R
+      auto taps = [&](const P* w, const T* s, int q, P* tz, P* tx) {
         const P uc = w[q + R];
         const T* row = s + (q + R) * SW;
         P xm[R + 1], xp[R + 1];
@@ -666,15 +724,52 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
           xm[4] = m4;
           xp[4] = p4;
         }
+#pragma unroll
+        for (int kk = 1; kk <= R; ++kk) {
+          tz[kk] = (w[q + R - kk] - uc) + (w[q + R + kk] - uc);
+          tx[kk] = (xm[kk] - uc) + (xp[kk] - uc);
+        }
+      };
+      auto lap2 = [&](const P* w, const T* s, int q) -> P {
+        P tz[R + 1], tx[R + 1];
+        taps(w, s, q, tz, tx);
         P lz = P::make(T(0), T(0)), lx = P::make(T(0), T(0));
 #pragma unroll
         for (int kk = 1; kk <= R; ++kk) {
           const P cz = P::make(a.cz[kk], a.cz[kk]);
           const P cx = P::make(a.cx[kk], a.cx[kk]);
-          lz = P::fma(cz, (w[q + R - kk] - uc) + (w[q + R + kk] - uc), lz);
-          lx = P::fma(cx, (xm[kk] - uc) + (xp[kk] - uc), lx);
+          lz = P::fma(cz, tz[kk], lz);
+          lx = P::fma(cx, tx[kk], lx);
         }
         return lz + lx;
+      };
+      // Laplacian of the forward recursion.  SG_GC (fp32): weights as ratios
+      // r_k = c_k / c_1 (r_1 = 1; hi + lo where not exact) and the x/z scale
+      // ratio rho as hi + lo -- no coherent weight rounding; the result is
+      // L u / K
+      auto lapf = [&](const P* w, const T* s, int q) -> P {
+        if constexpr (!GC) {
+          return lap2(w, s, q);
+        } else {
+          P tz[R + 1], tx[R + 1];
+          taps(w, s, q, tz, tx);
+          P lz = tz[1], lx = tx[1];
+#pragma unroll
+          for (int kk = 2; kk <= R; ++kk) {
+            const P rh = P::make(a.rh[kk], a.rh[kk]);
+            lz = P::fma(rh, tz[kk], lz);
+            lx = P::fma(rh, tx[kk], lx);
+            if (kk >= 3) {  // r_2 = -1/8 is exact (host checks rl[2] == 0)
+              const P rl = P::make(a.rl[kk], a.rl[kk]);
+              lz = P::fma(rl, tz[kk], lz);
+              lx = P::fma(rl, tx[kk], lx);
+            }
+          }
+          // (the z scale K rides in the model plane: accel multiplies by K/m)
+          if (a.iso) return lz + lx;
+          const P rhoh = P::make(a.rhoh, a.rhoh), rhol = P::make(a.rhol, a.rhol);
+          return P::fma(rhoh, lx, P::fma(rhol, lx, lz));
+        }
       };
       // forward acceleration a_n of the pair from its Laplacian (+ point source)
       auto accel = [&](P lp, int q) -> P {
@@ -702,8 +797,27 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
 
       // FULL: all kNY rows and both columns valid (interior tiles) -- no
       // per-row tests, unmasked pair stores
-      auto rows = [&](auto full_tag) {
+      auto rows = [&](auto full_tag, auto damp_tag) {
         constexpr bool FULL = decltype(full_tag)::value;
+        constexpr bool DAMP = decltype(damp_tag)::value;
+        // inc_{n+1} = d (inc_n + dt^2 a_n) and u_{n+1} = d u_n + inc_{n+1}
+        // (SG_GC: dt^2 as hi + lo, d x as x - e x with dd = -e; interior
+        // tiles: d = 1)
+        auto inc_next = [&](P acc, P sv, int q) -> P {
+          if constexpr (GCD) {
+            const P t = P::fma(dt2p, acc, P::fma(dt2lp, acc, sv));
+            if constexpr (!DAMP) return t;
+            else return P::fma(dd[q], t, t);
+          } else {
+            if constexpr (!DAMP) return P::fma(dt2p, acc, sv);
+            else return P::fma(dt2p, acc, sv) * dd[q];
+          }
+        };
+        auto u_next = [&](P uc, P so, int q) -> P {
+          if constexpr (!DAMP) return uc + so;
+          else if constexpr (GCD) return P::fma(dd[q], uc, uc) + so;
+          else return P::fma(dd[q], uc, so);
+        };
         auto put = [&](T* p, P v) {  // store a pair (only the valid half at the edge)
           if (FULL || vj1) st2(p, v);
           else p[0] = v.lo();
@@ -721,12 +835,12 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
 #pragma unroll
           for (int q = 0; q < kNY; ++q) {
             if (!FULL && q >= nq) continue;
-            const P acc = accel(lap2(colu, scu, q), q);
+            const P acc = accel(lapf(colu, scu, q), q);
             accs[q] = acc;
             if (HIST) put(hout + q * ldx, acc);
-            const P so = P::fma(dt2p, acc, lds2(sinc + q * kBX)) * dd[q];
+            const P so = inc_next(acc, lds2(sinc + q * kBX), q);
             put(rsout + q * ldx, so);
-            put(rout + q * ldx, P::fma(dd[q], colu[q + R], so));
+            put(rout + q * ldx, u_next(colu[q + R], so, q));
           }
         }
         if constexpr (RB) {
@@ -736,14 +850,17 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
 #pragma unroll
           for (int q = 0; q < kNY; ++q) {
             if (!FULL && q >= nq) continue;
-            const P acc = accel(lap2(colu, scu, q), q);
+            const P acc = accel(lapf(colu, scu, q), q);
             accs[q] = acc;
             P um1;
             if constexpr ((FL & FL_REV3) != 0) {
               // three-level reversal: the stage's state tile is u_{n+1}
-              um1 = P::fma(dt2p, acc, (colu[q + R] + colu[q + R]) - lds2(sinc + q * kBX));
+              um1 = (colu[q + R] + colu[q + R]) - lds2(sinc + q * kBX);
+              if constexpr (GC) um1 = P::fma(dt2lp, acc, um1);
+              um1 = P::fma(dt2p, acc, um1);
             } else {
-              const P incn = lds2(sinc + q * kBX) - dt2p * acc;
+              P incn = lds2(sinc + q * kBX) - dt2p * acc;
+              if constexpr (GC) incn = incn - dt2lp * acc;
               put(rsout + q * ldx, incn);
               um1 = colu[q + R] - incn;
             }
@@ -767,7 +884,7 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
         if (!FULL && q >= nq) continue;
         const P ucs = col[q + R];
         const P sv = lds2(sst + q * kBX);
-        P lp = lap2(col, sc, q);
+        P lp = ADJ ? lap2(col, sc, q) : lapf(col, sc, q);
         if (!ADJ) {
           if (GSRC) lp = P::fma(ldg2(gin + q * ldx), ldg2(a.gscale + o0 + q * ldx), lp);
           // LOCK: the scattered step, driven by the background's a0_n
@@ -781,9 +898,9 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
             if (bi1 >= 0) bdst[bi1] = ucs.hi();
           }
           if (HIST && !LOCK) put(hout + q * ldx, acc);
-          const P so = P::fma(dt2p, acc, sv) * dd[q];
+          const P so = inc_next(acc, sv, q);
           put(sout + q * ldx, so);
-          put(fout + q * ldx, P::fma(dd[q], ucs, so));
+          put(fout + q * ldx, u_next(ucs, so, q));
         } else {
           if (inj_here) {
             const int rr = ib + q - a.inj_row0;
@@ -813,12 +930,17 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
             // - d^2 lam_{n+2} + R^T y_n, v_n = coef lam_{n+1}) in V = coef lam:
             //   V_{n-1} = coef (L V_n + R^T y_n) + d (2 V_n - d V_{n+1});
             // sv is V_{n+1} (the tile of f[cur ^ 1], overwritten in place)
-            const P cf = (dt2p * im[q]) * dd[q];
-            put(fout + q * ldx, P::fma(cf, lp, dd[q] * ((ucs + ucs) - dd[q] * sv)));
+            if constexpr (!DAMP) {
+              put(fout + q * ldx, P::fma(cdt2p * im[q], lp, (ucs + ucs) - sv));
+            } else {
+              const P cf = (cdt2p * im[q]) * dd[q];
+              put(fout + q * ldx, P::fma(cf, lp, dd[q] * ((ucs + ucs) - dd[q] * sv)));
+            }
           } else {
-            const P so = P::fma(dd[q], sv, lp);
+            const P so = DAMP ? P::fma(dd[q], sv, lp) : sv + lp;
             put(sout + q * ldx, so);
-            put(fout + q * ldx, P::fma(dd[q], ucs, ((dt2p * im[q]) * dd[q]) * so));
+            if constexpr (!DAMP) put(fout + q * ldx, P::fma(cdt2p * im[q], so, ucs));
+            else put(fout + q * ldx, P::fma(dd[q], ucs, ((cdt2p * im[q]) * dd[q]) * so));
           }
           T v0, v1;
           ucs.split(v0, v1);
@@ -835,8 +957,10 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
         }
       }
       };
-      if (nq == kNY && vj1) rows(std::true_type{});
-      else rows(std::false_type{});
+      constexpr bool INNER = SG_INNER && !RB && (SG_INNER_LOCK || !LOCK);
+      if (INNER && tile_inner) rows(std::true_type{}, std::false_type{});
+      else if (nq == kNY && vj1) rows(std::true_type{}, std::true_type{});
+      else rows(std::false_type{}, std::true_type{});
     }
     __syncthreads();  // stage (k % NS) is free for shot k + NS
   }

@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -37,6 +38,73 @@
 namespace sg {
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
+
+// ---- red-zone allocator (SG_REDZONE=1; see sg_common.cuh) -------------------
+constexpr size_t kRedZone = 64 << 10;
+struct RzRec {
+  void* base;
+  size_t bytes;
+};
+static std::mutex g_rz_mu;
+static std::map<void*, RzRec> g_rz_live;       // user pointer -> allocation
+static std::atomic<int64_t> g_rz_bad{0};       // corrupted guard bytes found at free time
+static std::atomic<int64_t> g_rz_allocs{0};    // guarded allocations made so far
+
+static bool rz_on() {
+  static const bool on = [] {
+    const char* e = getenv("SG_REDZONE");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
+
+// guard bytes of one allocation that no longer hold 0xFF
+static int64_t rz_scan(const RzRec& r) {
+  std::vector<unsigned char> hbuf(2 * kRedZone);
+  cudaDeviceSynchronize();
+  if (cudaMemcpy(hbuf.data(), r.base, kRedZone, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(hbuf.data() + kRedZone, (char*)r.base + kRedZone + r.bytes, kRedZone,
+                 cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  int64_t bad = 0;
+  for (unsigned char c : hbuf) bad += c != 0xFF;
+  return bad;
+}
+
+cudaError_t rz_malloc(void** p, size_t bytes) {
+  if (!rz_on()) return cudaMalloc(p, bytes);
+  const size_t padded = (bytes + 255) / 256 * 256;  // keeps the tail zone aligned
+  void* base = nullptr;
+  cudaError_t e = cudaMalloc(&base, padded + 2 * kRedZone);
+  if (e != cudaSuccess) return e;
+  e = cudaMemset(base, 0xFF, padded + 2 * kRedZone);
+  if (e != cudaSuccess) {
+    cudaFree(base);
+    return e;
+  }
+  *p = (char*)base + kRedZone;
+  std::lock_guard<std::mutex> lk(g_rz_mu);
+  g_rz_live[*p] = RzRec{base, padded};
+  g_rz_allocs.fetch_add(1);
+  return cudaSuccess;
+}
+
+void rz_free(void* p) {
+  if (!p) return;
+  if (rz_on()) {
+    std::lock_guard<std::mutex> lk(g_rz_mu);
+    auto it = g_rz_live.find(p);
+    if (it != g_rz_live.end()) {
+      g_rz_bad.fetch_add(rz_scan(it->second));
+      cudaFree(it->second.base);
+      g_rz_live.erase(it);
+      return;
+    }
+  }
+  cudaFree(p);
+}
 }  // namespace sg
 
 using namespace sg;
@@ -70,16 +138,17 @@ EncodeTiledFn encode_fn() {
 // small kernels
 // ---------------------------------------------------------------------------
 
-// 1/m on the padded grid with edge replication (seisopt/wavesim.py:126-128,200-201)
+// scale/m on the padded grid with edge replication (seisopt/wavesim.py:126-128,200-201;
+// scale = 1, or the stencil's z scale K for the fp32 SG_GC forward)
 template <typename T, typename M>
 __global__ void k_set_inv_m(const M* __restrict__ m, T* __restrict__ inv_m, int nz, int nx,
-                            int nzp, int nxp, int ldx, int top, int left) {
+                            int nzp, int nxp, int ldx, int top, int left, double scale) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
   if (j >= nxp || i >= nzp) return;
   const int si = min(max(i - top, 0), nz - 1);
   const int sj = min(max(j - left, 0), nx - 1);
-  inv_m[i * ldx + j] = (T)(1.0 / (double)m[(int64_t)si * nx + sj]);
+  inv_m[i * ldx + j] = (T)(scale / (double)m[(int64_t)si * nx + sj]);
 }
 
 // edge-replicated, scaled copy onto the padded grid (Born scale -m_r_pad,
@@ -254,6 +323,9 @@ struct sg_handle {
   int tiles_x = 0, ntiles = 0, rec_blocks = 0;
   int ntiles2 = 0;  // tiles of the two-step kernel (64 x kTH2)
   double cz[5] = {0}, cx[5] = {0};
+  // SG_GC (fp32): the z scale K = c_1/dz^2 folded into the model plane
+  // (K/m), the source weights and the Born scale (/K); 1 otherwise
+  double kfold = 1.0;
   cudaStream_t stream = 0;
   cudaStream_t cap = nullptr;
   static constexpr int kMaxChains = 4;
@@ -264,6 +336,8 @@ struct sg_handle {
   void* inv_m_buf = nullptr;  // plane + tail
   void* pz_buf = nullptr;
   void* px_buf = nullptr;
+  void* ez_buf = nullptr;  // 1 - pz, 1 - px rounded from fp64 (SG_GC forward)
+  void* ex_buf = nullptr;
   void* gscale_buf = nullptr;  // -m_r on the padded grid (Born)
   int* src_rc = nullptr;  // (n_shots, 4, 2) tap rows/cols
   void* src_w = nullptr;
@@ -342,7 +416,7 @@ size_t span_bytes(const sg_handle* h, int cnt) {  // lead + cnt planes
 
 int dalloc(sg_handle* h, void** p, size_t bytes) {
   if (bytes == 0) bytes = 16;
-  cudaError_t e = cudaMalloc(p, bytes);
+  cudaError_t e = rz_malloc(p, bytes);
   if (e != cudaSuccess) {
     cudaGetLastError();
     *p = nullptr;
@@ -355,7 +429,7 @@ int dalloc(sg_handle* h, void** p, size_t bytes) {
 }
 
 void dfree(void** p) {
-  if (*p) cudaFree(*p);
+  if (*p) rz_free(*p);
   *p = nullptr;
 }
 
@@ -578,10 +652,22 @@ int step_args(sg_handle* h, StepArgs<T>& a, void* F0, void* F1, void* S0, void* 
   a.ntiles = h->ntiles;
   a.G = h->G;
   a.dt2 = (T)(h->d.dt * h->d.dt);
+  a.dt2l = (T)(h->d.dt * h->d.dt - (double)a.dt2);
   for (int k = 0; k < 5; ++k) {
     a.cz[k] = (T)h->cz[k];
     a.cx[k] = (T)h->cx[k];
   }
+  // exact-constant forward (SG_GC): ratios to c_1 and the axis scales, hi + lo
+  auto split = [](double v, T& hi, T& lo) {
+    hi = (T)v;
+    lo = (T)(v - (double)hi);
+  };
+  for (int k = 1; k < 5; ++k) split(h->cz[1] != 0.0 ? h->cz[k] / h->cz[1] : 0.0, a.rh[k], a.rl[k]);
+  split(h->cx[1] / h->cz[1], a.rhoh, a.rhol);
+  a.iso = (a.rhoh == (T)1 && a.rhol == (T)0) ? 1 : 0;
+  a.cdt2 = (T)(h->d.dt * h->d.dt / h->kfold);
+  a.ez = reinterpret_cast<const T*>(h->ez_buf) + kGuard;
+  a.ex = reinterpret_cast<const T*>(h->ex_buf) + kGuard;
   a.rec_ij = h->rec_ij;
   a.rec_w = reinterpret_cast<const T*>(h->rec_w);
   a.nrec = h->d.n_rec;
@@ -1809,7 +1895,7 @@ int set_born_scale(sg_handle* h, const void* m_r) {
   k_extend<T, T><<<grid, 128, 0, h->stream>>>(reinterpret_cast<const T*>(m_r),
                                               field<T>(h->gscale_buf, h), h->d.nz, h->d.nx,
                                               h->nzp, h->nxp, h->ldx, h->d.pad_top,
-                                              h->d.pad_left, -1.0);
+                                              h->d.pad_left, -1.0 / h->kfold);
   count_launch();
   SG_CK(cudaGetLastError());
   return SG_OK;
@@ -2051,7 +2137,7 @@ int forward_history_t(sg_handle* h, int shot, void* gather, void* accel) {
                                             (int64_t)nt * h->nzp, h->nxp, h->ldx);
   count_launch();
   SG_CK(cudaStreamSynchronize(h->stream));
-  cudaFree(tmp);
+  rz_free(tmp);
   h->held_bytes -= (double)nt * h->hplane * h->esz;
   return SG_OK;
 }
@@ -2074,7 +2160,7 @@ int adjoint_history_t(sg_handle* h, const void* ybar, void* vout) {
                                             (int64_t)nt * h->nzp, h->nxp, h->ldx);
   count_launch();
   SG_CK(cudaStreamSynchronize(h->stream));
-  cudaFree(tmp);
+  rz_free(tmp);
   h->held_bytes -= (double)nt * h->hplane * h->esz;
   return SG_OK;
 }
@@ -2181,6 +2267,24 @@ int sg_version(void) { return 2; }
 int sg_build_flags(void) { return SG_EXPERIMENTAL ? SG_BUILD_EXPERIMENTAL : 0; }
 int64_t sg_launch_count(void) { return sg::g_launches.load(); }
 
+int sg_redzone_check(int64_t* bad_bytes, int64_t* allocations, int32_t poke) {
+  if (!bad_bytes || !allocations) return fail(SG_ERR_ARG, "null argument");
+  *bad_bytes = 0;
+  *allocations = 0;
+  if (!sg::rz_on()) return SG_OK;
+  std::lock_guard<std::mutex> lk(sg::g_rz_mu);
+  if (poke && !sg::g_rz_live.empty()) {
+    // self-test: one byte written just past the first live allocation
+    const auto& r = sg::g_rz_live.begin()->second;
+    SG_CK(cudaMemset((char*)r.base + sg::kRedZone + r.bytes, 0, 1));
+  }
+  int64_t bad = sg::g_rz_bad.load();
+  for (const auto& kv : sg::g_rz_live) bad += sg::rz_scan(kv.second);
+  *bad_bytes = bad;
+  *allocations = sg::g_rz_allocs.load();
+  return SG_OK;
+}
+
 int sg_create(const sg_desc* d, sg_handle** out) {
   if (!d || !out) return fail(SG_ERR_ARG, "null argument");
   *out = nullptr;
@@ -2224,6 +2328,7 @@ int sg_create(const sg_desc* d, sg_handle** out) {
       h->cx[k] = c8[k] * rx;
     }
   }
+  if (SG_GC && h->esz == 4) h->kfold = h->cz[1];
   int rc = dalloc(h, &h->inv_m_buf, (size_t)(h->ldx + h->plane + h->tail) * h->esz);
   if (rc) {
     delete h;
@@ -2238,7 +2343,7 @@ int sg_destroy(sg_handle* h) {
   cudaSetDevice(h->d.device);
   free_batch(h);
   void** bufs[] = {(void**)&h->rec_rc, (void**)&h->tile_rec_ptr, (void**)&h->tile_rec,
-                   &h->inv_m_buf, &h->pz_buf, &h->px_buf, &h->gscale_buf, (void**)&h->src_rc,
+                   &h->inv_m_buf, &h->pz_buf, &h->px_buf, &h->ez_buf, &h->ex_buf, &h->gscale_buf, (void**)&h->src_rc,
                    &h->src_w, (void**)&h->rec_ij, &h->rec_w, (void**)&h->inj_ptr,
                    (void**)&h->inj_rec, &h->inj_w, &h->born_hist, &h->wav_dev,
                    (void**)&h->res_rec};
@@ -2270,7 +2375,11 @@ int sg_set_sponge(sg_handle* h, const double* pz, const double* px) {
   for (int j = 0; j < h->nxp; ++j) x[kGuard + j] = px[j];
   // frame of the band store: every row/column whose profile (in the device
   // dtype) is below 1 at either end, i.e. every cell with damp < 1
-  auto below1 = [&](double v) { return h->esz == 4 ? (float)v < 1.0f : v < 1.0; };
+  // (fp32 with SG_GC damps by e = (float)(1 - p): the same rows/columns
+  // unless p is within 2^-25 of 1, so both tests are applied)
+  auto below1 = [&](double v) {
+    return h->esz == 4 ? ((float)v < 1.0f || (float)(1.0 - v) > 0.0f) : v < 1.0;
+  };
   auto frame = [&](const double* p, int n, int& lo, int& hi) {
     lo = 0;
     hi = 0;
@@ -2290,12 +2399,22 @@ int sg_set_sponge(sg_handle* h, const double* pz, const double* px) {
   free_batch(h);  // batch buffers are sized with the frame
   dfree(&h->pz_buf);
   dfree(&h->px_buf);
+  dfree(&h->ez_buf);
+  dfree(&h->ex_buf);
+  // e = 1 - p in fp64, rounded once (zero guards and tails stay zero)
+  std::vector<double> ezv(z.size(), 0.0), exv(x.size(), 0.0);
+  for (int i = 0; i < h->nzp; ++i) ezv[kGuard + i] = 1.0 - pz[i];
+  for (int j = 0; j < h->nxp; ++j) exv[kGuard + j] = 1.0 - px[j];
   if (h->esz == 4) {
     SG_TRY(upload_cast<float>(h, &h->pz_buf, z.data(), z.size()));
     SG_TRY(upload_cast<float>(h, &h->px_buf, x.data(), x.size()));
+    SG_TRY(upload_cast<float>(h, &h->ez_buf, ezv.data(), ezv.size()));
+    SG_TRY(upload_cast<float>(h, &h->ex_buf, exv.data(), exv.size()));
   } else {
     SG_TRY(upload_cast<double>(h, &h->pz_buf, z.data(), z.size()));
     SG_TRY(upload_cast<double>(h, &h->px_buf, x.data(), x.size()));
+    SG_TRY(upload_cast<double>(h, &h->ez_buf, ezv.data(), ezv.size()));
+    SG_TRY(upload_cast<double>(h, &h->ex_buf, exv.data(), exv.size()));
   }
   h->have_sponge = true;
   return SG_OK;
@@ -2319,7 +2438,7 @@ int sg_set_geometry(sg_handle* h, const int32_t* src_rows, const int32_t* src_co
       if (!in_grid(r, c)) return fail(SG_ERR_ARG, "source tap outside padded grid");
       src[(s * 4 + k) * 2] = r;
       src[(s * 4 + k) * 2 + 1] = c;
-      sw[s * 4 + k] = src_w[k * S + s] * src_scale;
+      sw[s * 4 + k] = src_w[k * S + s] * src_scale / h->kfold;
     }
   std::vector<int> rij(4 * R);
   int rmin = 1 << 30, rmax = -1;
@@ -2455,14 +2574,14 @@ int sg_set_model(sg_handle* h, const void* m, int32_t mdt) {
   dim3 grid(cdiv(h->nxp, 128), h->nzp);
   if (h->esz == 4) {
     if (mdt == SG_F32)
-      k_set_inv_m<float, float><<<grid, 128, 0, h->stream>>>((const float*)m, field<float>(h->inv_m_buf, h), h->d.nz, h->d.nx, h->nzp, h->nxp, h->ldx, h->d.pad_top, h->d.pad_left);
+      k_set_inv_m<float, float><<<grid, 128, 0, h->stream>>>((const float*)m, field<float>(h->inv_m_buf, h), h->d.nz, h->d.nx, h->nzp, h->nxp, h->ldx, h->d.pad_top, h->d.pad_left, h->kfold);
     else
-      k_set_inv_m<float, double><<<grid, 128, 0, h->stream>>>((const double*)m, field<float>(h->inv_m_buf, h), h->d.nz, h->d.nx, h->nzp, h->nxp, h->ldx, h->d.pad_top, h->d.pad_left);
+      k_set_inv_m<float, double><<<grid, 128, 0, h->stream>>>((const double*)m, field<float>(h->inv_m_buf, h), h->d.nz, h->d.nx, h->nzp, h->nxp, h->ldx, h->d.pad_top, h->d.pad_left, h->kfold);
   } else {
     if (mdt == SG_F32)
-      k_set_inv_m<double, float><<<grid, 128, 0, h->stream>>>((const float*)m, field<double>(h->inv_m_buf, h), h->d.nz, h->d.nx, h->nzp, h->nxp, h->ldx, h->d.pad_top, h->d.pad_left);
+      k_set_inv_m<double, float><<<grid, 128, 0, h->stream>>>((const float*)m, field<double>(h->inv_m_buf, h), h->d.nz, h->d.nx, h->nzp, h->nxp, h->ldx, h->d.pad_top, h->d.pad_left, h->kfold);
     else
-      k_set_inv_m<double, double><<<grid, 128, 0, h->stream>>>((const double*)m, field<double>(h->inv_m_buf, h), h->d.nz, h->d.nx, h->nzp, h->nxp, h->ldx, h->d.pad_top, h->d.pad_left);
+      k_set_inv_m<double, double><<<grid, 128, 0, h->stream>>>((const double*)m, field<double>(h->inv_m_buf, h), h->d.nz, h->d.nx, h->nzp, h->nxp, h->ldx, h->d.pad_top, h->d.pad_left, h->kfold);
   }
   count_launch();
   SG_CK(cudaGetLastError());

@@ -6,6 +6,7 @@ C3 gradient, and the NCCL all-reduce path of the shot scheduler
 (shards.ShotShard) on one rank.
 """
 
+import os
 import socket
 
 import numpy as np
@@ -156,3 +157,22 @@ def test_nccl_allreduce_path_one_rank():
     assert torch.equal(g0, g1)
     assert abs(v1 - v0) <= 1e-15 * abs(v0)
     assert abs(j1 - j0) <= 1e-15 * abs(j0)
+
+
+def test_redzone_memcheck_small_sweeps():
+    """The library's own memcheck (compute-sanitizer is refused on this GPU
+    pool): every sweep flavour of the small 60 x 40 case -- fp32/fp64, FULL /
+    CHECKPOINT / BOUNDARY, two chains, PDL, Born cached and lock-step, AA window
+    -- on guarded allocations (SG_REDZONE=1: 64 KB of NaN bytes around every
+    device buffer).  No guard byte may change and every result stays finite;
+    a deliberate one-byte overrun is detected.  Plain launches and graphs."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SG_REDZONE="1")
+    for extra in ([], ["--graphs"]):
+        r = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize_case.py"),
+                            "--redzone", *extra], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        assert "0 guard bytes modified; self-test poke found" in r.stdout
