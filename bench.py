@@ -127,8 +127,10 @@ def clock_sampler(index):
 
 def l2_cap_gbs(clocks):
     """L2 (LTS) throughput cap: ~6300 B/cycle full chip (measured,
-    /opt/skills/guides/B300_MICROARCH.md) at the SM clock this run sampled."""
-    mhz = (clocks or {}).get("sm_mhz")
+    /opt/skills/guides/B300_MICROARCH.md) at the maximum SM clock.  Under the
+    power cap the SM clock this run samples is lower, and the measured L2
+    rate then exceeds 6300 B x that clock, so the L2 does not follow it."""
+    mhz = (clocks or {}).get("sm_max_mhz")
     return 6300.0 * mhz * 1e6 / 1e9 if mhz else None
 
 
@@ -649,7 +651,7 @@ def run_ours(args):
                       "traffic_gbs": (tr / (msk / 1e3) / 1e9) if tr else None,
                       # L2 tag-stage bytes (ncu lts__t_bytes.sum, steady state) over
                       # the live step time, against the measured LTS cap of
-                      # ~6300 B/cycle at the SM clock sampled in this run
+                      # ~6300 B/cycle at the maximum SM clock
                       "l2_bytes_per_step": lts,
                       "l2_gbs": (lts / (msk / 1e3) / 1e9) if lts else None,
                       "l2_frac": (lts / (msk / 1e3) / 1e9 / l2_cap) if (lts and l2_cap) else None,
@@ -709,7 +711,7 @@ def run_ours(args):
                          "traffic_frac": (dk["traffic_gbs"] / peak) if dk["traffic_gbs"] else None,
                          "l2": {"gbs": dk["l2_gbs"], "cap_gbs": l2_cap, "frac": dk["l2_frac"],
                                 "cap_source": "6300 B/cycle (B300_MICROARCH.md LTS cap) x "
-                                              "sampled SM clock"},
+                                              "max SM clock"},
                          "shots_per_step": launch_shots,
                          "chains": prop.chains(launch_shots),
                          "bytes_per_step": dk["bytes_per_step"], "ms_per_step": dk["ms_per_step"],

@@ -217,6 +217,13 @@ int sg_phase_times(sg_handle* h, float* ms_out);
 /* Number of kernel launches this handle (or AA window) has issued. */
 int64_t sg_launch_count(void);
 
+/* NaN/Inf guard: the number of non-finite entries in the gradient
+ * or image the last sg_fwi_gradient / sg_lsrtm_gradient / sg_born_adjoint on
+ * this handle wrote (counted on the device while folding the result).  The
+ * reference raises nothing for a diverged sweep; the Python layer turns a
+ * non-zero count into a RuntimeWarning.  No reference counterpart. */
+int sg_last_nonfinite(sg_handle* h, int64_t* count);
+
 /* The library's own memcheck.  With SG_REDZONE=1 in the environment when the
  * library is loaded, every device allocation of a handle or AA window carries
  * 64 KB guard zones of 0xFF bytes (NaN in fp32 and fp64) on both sides: an

@@ -86,6 +86,7 @@ SIGNATURES = {
     "sg_time_step_kernel": (C.c_int, [_P, _I32, _I32, _I32, C.POINTER(C.c_float)]),
     "sg_phase_times": (C.c_int, [_P, C.POINTER(C.c_float)]),
     "sg_launch_count": (C.c_int64, []),
+    "sg_last_nonfinite": (C.c_int, [_P, C.POINTER(C.c_int64)]),
     "sg_redzone_check": (C.c_int, [C.POINTER(C.c_int64), C.POINTER(C.c_int64), _I32]),
     "sg_aa_create": (C.c_int, [_I64, _I32, _I32, _I32, C.POINTER(_P)]),
     "sg_aa_destroy": (C.c_int, [_P]),

@@ -264,7 +264,8 @@ __global__ void k_reduce_images(const T* __restrict__ img, T* __restrict__ acc, 
 // fold_pad: transpose of edge replication (seisopt/wavesim.py:135-147)
 template <typename T>
 __global__ void k_fold(const T* __restrict__ pad, T* __restrict__ out, int nz, int nx,
-                       int nzp, int nxp, int ldx, int top, int left, int accumulate) {
+                       int nzp, int nxp, int ldx, int top, int left, int accumulate,
+                       double* __restrict__ nonfinite) {
   const int ix = blockIdx.x * blockDim.x + threadIdx.x;
   const int iz = blockIdx.y;
   if (ix >= nx) return;
@@ -280,6 +281,9 @@ __global__ void k_fold(const T* __restrict__ pad, T* __restrict__ out, int nz, i
   }
   const int64_t o = (int64_t)iz * nx + ix;
   out[o] = accumulate ? out[o] + s : s;
+  // NaN/Inf guard of the result (a diverged sweep): counted, reported by
+  // sg_last_nonfinite
+  if (!isfinite((double)s)) atomicAdd(nonfinite, 1.0);
 }
 
 // compact (rows x nxp) <- pitched (rows x ldx)
@@ -326,6 +330,9 @@ struct sg_handle {
   // SG_GC (fp32): the z scale K = c_1/dz^2 folded into the model plane
   // (K/m), the source weights and the Born scale (/K); 1 otherwise
   double kfold = 1.0;
+  // NaN/Inf entries of the last folded gradient / image (sg_last_nonfinite)
+  double nonfinite = 0.0;
+  bool nonfinite_pending = false;
   cudaStream_t stream = 0;
   cudaStream_t cap = nullptr;
   static constexpr int kMaxChains = 4;
@@ -1349,12 +1356,16 @@ int reduce_images(sg_handle* h, int cnt) {
 template <typename T>
 int fold_out(sg_handle* h, void* out, int accumulate) {
   dim3 grid(cdiv(h->d.nx, 128), h->d.nz);
+  double* nf = h->scal + 8;  // non-finite entries of this output
+  SG_CK(cudaMemsetAsync(nf, 0, sizeof(double), h->stream));
   k_fold<T><<<grid, 128, 0, h->stream>>>(reinterpret_cast<const T*>(h->acc_img),
                                          reinterpret_cast<T*>(out), h->d.nz, h->d.nx, h->nzp,
                                          h->nxp, h->ldx, h->d.pad_top, h->d.pad_left,
-                                         accumulate);
+                                         accumulate, nf);
   count_launch();
   SG_CK(cudaGetLastError());
+  SG_CK(cudaMemcpyAsync(&h->nonfinite, nf, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  h->nonfinite_pending = true;
   return SG_OK;
 }
 
@@ -2266,6 +2277,17 @@ const char* sg_last_error(void) { return sg::g_err.c_str(); }
 int sg_version(void) { return 2; }
 int sg_build_flags(void) { return SG_EXPERIMENTAL ? SG_BUILD_EXPERIMENTAL : 0; }
 int64_t sg_launch_count(void) { return sg::g_launches.load(); }
+
+int sg_last_nonfinite(sg_handle* h, int64_t* count) {
+  SG_TRY(check_handle(h));
+  if (!count) return fail(SG_ERR_ARG, "null argument");
+  if (h->nonfinite_pending) {
+    SG_CK(cudaStreamSynchronize(h->stream));
+    h->nonfinite_pending = false;
+  }
+  *count = (int64_t)h->nonfinite;
+  return SG_OK;
+}
 
 int sg_redzone_check(int64_t* bad_bytes, int64_t* allocations, int32_t poke) {
   if (!bad_bytes || !allocations) return fail(SG_ERR_ARG, "null argument");

@@ -19,6 +19,7 @@ import ctypes as C
 import hashlib
 import math
 import threading
+import warnings
 from collections import OrderedDict
 from dataclasses import dataclass
 
@@ -206,6 +207,19 @@ class Propagator:
             return x.to(device=self.device, dtype=dt).contiguous()
         return torch.as_tensor(np.ascontiguousarray(x), device=self.device, dtype=dt)
 
+    def _guard(self, what, value=None):
+        """NaN/Inf guard: warn when the sweep diverged.  The
+        reference returns the NaNs silently; so does this (same values), but
+        says so."""
+        n = C.c_int64()
+        _lib.check(self.lib.sg_last_nonfinite(self.h, C.byref(n)), "last_nonfinite")
+        self.last_nonfinite = n.value
+        bad_val = value is not None and not np.isfinite(value)
+        if n.value or bad_val:
+            warnings.warn(f"{what}: non-finite result ({n.value} gradient entries"
+                          f"{', misfit ' + repr(value) if bad_val else ''}): the sweep diverged",
+                          RuntimeWarning, stacklevel=3)
+
     def close(self):
         if getattr(self, "h", None):
             self.lib.sg_destroy(self.h)
@@ -267,6 +281,7 @@ class Propagator:
         self._stream()
         _lib.check(self.lib.sg_fwi_gradient(self.h, s0, cnt, _lib.dptr(obs), C.byref(v),
                                             _lib.dptr(out), 1 if accumulate else 0), "gradient")
+        self._guard("fwi_gradient", v.value)
         return v.value, out
 
     def born_cache(self, shots=None, enable=True):
@@ -299,6 +314,7 @@ class Propagator:
         self._stream()
         _lib.check(self.lib.sg_born_adjoint(self.h, s0, cnt, _lib.dptr(dd), _lib.dptr(out),
                                             1 if accumulate else 0), "born_adjoint")
+        self._guard("born_adjoint")
         return out
 
     def lsrtm_gradient(self, m_r, d_r, shots=None, out=None, accumulate=False):
@@ -313,6 +329,7 @@ class Propagator:
         _lib.check(self.lib.sg_lsrtm_gradient(self.h, s0, cnt, _lib.dptr(mr), _lib.dptr(dr),
                                               C.byref(v), _lib.dptr(out),
                                               1 if accumulate else 0), "lsrtm_gradient")
+        self._guard("lsrtm_gradient", v.value)
         return v.value, out
 
     def lsrtm_misfit(self, m_r, d_r, shots=None):

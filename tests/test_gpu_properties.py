@@ -176,3 +176,29 @@ def test_redzone_memcheck_small_sweeps():
                            timeout=600)
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
         assert "0 guard bytes modified; self-test poke found" in r.stdout
+
+
+def test_nonfinite_guard_warns():
+    """Device NaN/Inf guard: a gradient with non-finite entries
+    (here: a NaN in the observed data, as a diverged sweep would produce) is
+    counted on the device while folding and surfaces as a RuntimeWarning; a
+    clean gradient raises nothing and counts zero."""
+    import warnings
+
+    from paper_2008_11778_b200.model import SimConfig
+    from paper_2008_11778_b200.wavesim import Propagator
+    grid, geom, wav, m0, m_true = _fd_case()
+    prop = Propagator(grid, geom, wav, SimConfig(border_width=20, order=8), dtype="float32")
+    prop.set_model(m_true)
+    obs = prop.synthetic().clone()
+    prop.set_model(m0)
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        val, grad = prop.gradient(obs)
+    assert prop.last_nonfinite == 0 and np.isfinite(val)
+    obs[0, 5, 3] = float("nan")
+    with pytest.warns(RuntimeWarning, match="non-finite"):
+        val, grad = prop.gradient(obs)
+    assert prop.last_nonfinite > 0
+    assert not bool(torch.isfinite(grad).all())
+    prop.close()
