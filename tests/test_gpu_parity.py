@@ -265,6 +265,30 @@ def test_c1_fp32_gradient():
     assert rel(ev.gradient, g["grad"]) <= F32
 
 
+@pytest.mark.parametrize("order", [2, 8])
+@pytest.mark.parametrize("damp_top", [True, False])
+@pytest.mark.parametrize("recon", ["full", "checkpoint", "boundary"])
+def test_small_fp32_gradient_vs_reference(order, damp_top, recon):
+    """fp32 production path on the reference's own small 60 x 40 goldens
+    (gathers, misfit, FWI gradient, Born data and image): <= 1e-4 in every
+    reconstruction mode.  Round 1 missed this at 1.2e-4 on small_o8_top; the
+    exact-constant forward (SG_GC, DESIGN s4) brings it to ~2e-5."""
+    _, wavesim = _api()
+    case = small_case(order, damp_top)
+    g = case["gold"]
+    p = wavesim.Propagator(case["grid"], case["geometry"], case["wavelet"], case["config"],
+                           dtype="float32", recon=recon, checkpoint_every=38)
+    p.set_model(g["m"])
+    assert rel(p.synthetic().cpu().numpy(), g["syn"]) <= F32
+    v, gr = p.gradient(g["obs"])
+    assert abs(v - float(g["value"])) <= F32 * float(g["value"])
+    assert rel(gr.cpu().numpy(), g["grad"]) <= F32
+    if recon != "boundary":
+        assert rel(p.born_forward(g["m_r"]).cpu().numpy(), g["born"]) <= F32
+        assert rel(p.born_adjoint(g["y"]).cpu().numpy(), g["img"]) <= F32
+    p.close()
+
+
 def test_forward_and_adjoint_histories():
     _, wavesim = _api()
     case = small_case(8, True)
