@@ -755,44 +755,57 @@ def aa_stream_torch(n, count, seed, dev, dtype):
 def run_c2(args):
     """Standalone AA mixing step (configs[1]): N = 5e7 fp32, m = 10; one step =
     push (fused residual-difference + Gram row pass) + host m x m solve +
-    recombination, window full and sliding."""
+    recombination, window full and sliding.  On several GPUs N is sharded
+    (SURVEY s8e): each rank's window holds N / world entries and the Gram row
+    is summed over the ranks (one small all-reduce per push)."""
     import torch
 
-    from paper_2008_11778_b200 import _lib, anderson
+    from paper_2008_11778_b200 import _lib, anderson, shards
     rank, world, local = env_rank()
-    if rank != 0:
-        return 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    n, m = 50_000_000, 10
+    dist = init_dist(dev, world)
+    n_total, m = 50_000_000, 10
+    n0, n = shards.shard_bounds(n_total, world, rank)
     total = m + 1 + args.warmup + args.steps
-    stream = aa_stream_torch(n, total, 0, dev, torch.float32)
-    win = anderson.AAWindow(n, m, dtype="float32", device=dev)
+    stream = aa_stream_torch(n, total, rank, dev, torch.float32)
+    win = anderson.AAWindow(n, m, dtype="float32", device=dev,
+                            shard_group=True if dist is not None else None)
     out = torch.empty(n, device=dev, dtype=torch.float32)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
     for k in range(m + 1 + args.warmup):
         win.push(*stream[k])
         if win.m_k:
             anderson.aa_step(win, weights=anderson.aa_weights(win), out=out)
-    torch.cuda.synchronize()
+    barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = _lib.launch_count()
     with clock_sampler(local) as clk:
+        barrier()
         e0.record()
         for k in range(m + 1 + args.warmup, total):
             win.push(*stream[k])
             w = anderson.aa_weights(win)
             anderson.aa_step(win, weights=w, out=out)
         e1.record()
-        torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
+        barrier()
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
     launches = _lib.launch_count() - l0
-    alg_bytes = 4.0 * n * (2 * m + 7)  # SURVEY s8d byte model
+    alg_bytes = 4.0 * n_total * (2 * m + 7)  # SURVEY s8d byte model, all ranks
     peak, src = peaks()
     # e2e: host vectors in (pinned), host iterate out, every step
     hp = [(a.cpu().pin_memory(), b.cpu().pin_memory()) for a, b in stream[-args.steps:]]
     host_out = torch.empty(n, dtype=torch.float32).pin_memory()
     pd, gd = torch.empty_like(out), torch.empty_like(out)
-    torch.cuda.synchronize()
+    barrier()
     t0 = time.perf_counter()
     for a, b in hp:
         pd.copy_(a, non_blocking=True)
@@ -800,10 +813,14 @@ def run_c2(args):
         win.push(pd, gd)
         anderson.aa_step(win, weights=anderson.aa_weights(win), out=out)
         host_out.copy_(out, non_blocking=True)
-    torch.cuda.synchronize()
-    e2e_ms = (time.perf_counter() - t0) * 1e3 / len(hp)
+    barrier()
+    te = torch.tensor([(time.perf_counter() - t0) * 1e3 / len(hp)], dtype=torch.float64,
+                      device=dev)
+    if dist is not None:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item())
     cpu = None
-    if not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         import oracle
         nc = 5_000_000
         rng = np.random.default_rng(0)
@@ -815,27 +832,32 @@ def run_c2(args):
         for k in range(m + 1, m + 3):
             wo.push(*vecs[k])
             oracle.aa_step(wo, 1.0, oracle.aa_weights(wo))
-        cms = (time.perf_counter() - t0) * 1e3 / 2 * (n / nc)
+        cms = (time.perf_counter() - t0) * 1e3 / 2 * (n_total / nc)
         cpu = {"value": cms, "unit": "ms/iteration", "cores": os.cpu_count() or 1,
                "cpu_model": cpu_model(),
                "kind": "port", "sample": f"oracle AAWindow push+weights+step at N={nc}, m={m}, "
                                          "2 steady-state iterations, scaled x10 to N=5e7"}
-    line = {"metric": "AA mixing step time (push + weights + step)", "value": ms,
-            "unit": "ms/iteration", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "C2 standalone AA mixing step: N=5e7 fp32, m=10, N(0,1) + "
-                                   "rank-3 smooth component", "l2": "inputs larger than L2 "
-                                   "(%.1f GB of window vectors)" % (2 * m * n * 4 / 1e9)},
-            "e2e": {"value": e2e_ms, "unit": "ms/iteration", "h2d_bytes_per_step": 2 * n * 4,
-                    "d2h_bytes_per_step": n * 4},
-            "roofline": {"bound": "hbm", "kernel": "aa_push + aa_step",
-                         "achieved": alg_bytes / (ms / 1e3) / 1e9, "peak": peak,
-                         "peak_source": src, "unit": "GB/s",
-                         "frac": alg_bytes / (ms / 1e3) / 1e9 / peak, "traffic": None,
-                         "bytes_per_launch": alg_bytes},
-            "gpu_launches": launches, "clocks": clk.summary(), "cpu_baseline": cpu}
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        line = {"metric": "AA mixing step time (push + weights + step)", "value": ms,
+                "unit": "ms/iteration", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "C2 standalone AA mixing step: N=5e7 fp32, m=10, N(0,1) + "
+                                       "rank-3 smooth component", "n_per_rank": n,
+                           "l2": "inputs larger than L2 (%.1f GB of window vectors per rank)"
+                                 % (2 * m * n * 4 / 1e9)},
+                "e2e": {"value": e2e_ms, "unit": "ms/iteration", "h2d_bytes_per_step": 2 * n * 4,
+                        "d2h_bytes_per_step": n * 4},
+                "roofline": {"bound": "hbm", "kernel": "aa_push + aa_step",
+                             "achieved": alg_bytes / world / (ms / 1e3) / 1e9, "peak": peak,
+                             "peak_source": src, "unit": "GB/s",
+                             "frac": alg_bytes / world / (ms / 1e3) / 1e9 / peak, "traffic": None,
+                             "bytes_per_launch": alg_bytes / world},
+                "gpu_launches": launches, "clocks": clk.summary(), "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
     return 0
 
 

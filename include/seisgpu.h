@@ -250,6 +250,17 @@ int sg_redzone_check(int64_t* bad_bytes, int64_t* allocations, int32_t poke);
 int sg_aa_create(int64_t n, int32_t memory, int32_t dtype, int32_t device, sg_aa** out);
 int sg_aa_destroy(sg_aa* a);
 int sg_aa_set_stream(sg_aa* a, void* cuda_stream);
+/* N-sharded window (the standalone AA step on several GPUs shards
+ * N): each rank's window holds its slice of the N-vectors.  Every quantity
+ * the window reads back from the device -- Gram rows <df, dF_i>, projections
+ * <f_k, dF_i>, squared norms, the QR fallback's dots -- is a plain sum over
+ * the N entries, so `fn` only has to sum a small host buffer of doubles
+ * (<= 2m + 3 values) over the ranks in place (an all-reduce; 0 = success).
+ * gamma, alpha, the window decisions and the rank safeguard are then
+ * identical on every rank, as the replicated reference window's would be
+ * (seisopt/optim/anderson.py:55-123).  NULL restores the single-rank window. */
+typedef int (*sg_reduce_fn)(double* buf, int32_t n, void* ctx);
+int sg_aa_set_reducer(sg_aa* a, sg_reduce_fn fn, void* ctx);
 int sg_aa_clear(sg_aa* a);                                   /* anderson.py:77-78 */
 int sg_aa_push(sg_aa* a, const void* p_dev, const void* g_dev); /* anderson.py:80-112 */
 int sg_aa_m_k(sg_aa* a);                                     /* anderson.py:69-71 */

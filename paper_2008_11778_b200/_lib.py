@@ -91,6 +91,7 @@ SIGNATURES = {
     "sg_aa_create": (C.c_int, [_I64, _I32, _I32, _I32, C.POINTER(_P)]),
     "sg_aa_destroy": (C.c_int, [_P]),
     "sg_aa_set_stream": (C.c_int, [_P, _P]),
+    "sg_aa_set_reducer": (C.c_int, [_P, _P, _P]),
     "sg_aa_clear": (C.c_int, [_P]),
     "sg_aa_push": (C.c_int, [_P, _P, _P]),
     "sg_aa_m_k": (C.c_int, [_P]),
@@ -106,6 +107,9 @@ SIGNATURES = {
     "sg_vec_multi_dot": (C.c_int, [_I64, _I32, _I32, C.POINTER(_P), _P, _DP, _P]),
     "sg_vec_multi_axpy": (C.c_int, [_I64, _I32, _I32, _DP, C.POINTER(_P), _P, _P, _P]),
 }
+
+# sg_reduce_fn: int (*)(double* buf, int32_t n, void* ctx)
+REDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int32, C.c_void_p)
 
 _lock = threading.Lock()
 _lib = None

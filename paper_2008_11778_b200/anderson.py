@@ -89,7 +89,11 @@ class WeightSolution:
 class AAWindow:
     """Sliding AA history held on the GPU (seisopt/optim/anderson.py:55-112)."""
 
-    def __init__(self, dim, memory, dtype="float64", device=None, qr="auto"):
+    def __init__(self, dim, memory, dtype="float64", device=None, qr="auto", shard_group=None):
+        """``shard_group``: a torch.distributed process group (or True for the
+        default group) over which the N-vectors are sharded -- ``dim`` is then
+        this rank's slice length and every inner product of the window is
+        summed over the group (sg_aa_set_reducer)."""
         torch = _torch()
         if qr not in ("auto", "always"):
             raise ValueError("qr must be 'auto' (Gram, device QR when it cannot resolve "
@@ -111,6 +115,36 @@ class AAWindow:
         self._numpy_io = False
         if qr == "always":
             _lib.check(self.lib.sg_aa_set_qr(h, 1), "sg_aa_set_qr")
+        self._reducer = None
+        if shard_group is not None and shard_group is not False:
+            self._install_reducer(None if shard_group is True else shard_group)
+
+    def _install_reducer(self, group):
+        torch = _torch()
+        import torch.distributed as dist
+        if not (dist.is_available() and dist.is_initialized()):
+            raise RuntimeError("a sharded AAWindow needs an initialised process group")
+        if dist.get_world_size(group) == 1:
+            return
+        nccl = dist.get_backend(group) == "nccl"
+        dev = self.device
+
+        def reduce(buf, n, _ctx):
+            try:
+                host = torch.from_numpy(np.ctypeslib.as_array(buf, shape=(n,)))
+                if nccl:
+                    t = host.to(dev)
+                    dist.all_reduce(t, group=group)
+                    host.copy_(t)
+                else:
+                    dist.all_reduce(host, group=group)
+                return 0
+            except Exception:  # surfaces as SG_ERR_STATE from the push
+                return 1
+
+        self._reducer = _lib.REDUCE_FN(reduce)  # keep the thunk alive
+        _lib.check(self.lib.sg_aa_set_reducer(self.h, C.cast(self._reducer, C.c_void_p), None),
+                   "sg_aa_set_reducer")
 
     def __del__(self):
         try:

@@ -572,6 +572,9 @@ struct sg_aa {
   bool qr_active = false;
   std::vector<double> Rq;
   int64_t qr_passes = 0;  // device QR passes run (diagnostics)
+  // N-sharded windows: sums every device inner product over the ranks
+  sg_reduce_fn reduce = nullptr;
+  void* reduce_ctx = nullptr;
   // cached weights of the current window
   bool have_w = false;
   std::vector<double> gamma, alpha;
@@ -581,6 +584,15 @@ struct sg_aa {
 namespace {
 
 int slot_of(const sg_aa* a, int pos) { return (a->head + pos) % std::max(1, a->memory); }
+
+// Every quantity the window reads back from the device is a plain sum over
+// the N entries (Gram rows, projections, squared norms), so an N-sharded
+// window only has to sum these few doubles over the ranks (sg_aa_set_reducer)
+int reduce_sums(sg_aa* a, double* buf, int n) {
+  if (a->reduce && a->reduce(buf, n, a->reduce_ctx) != 0)
+    return fail(SG_ERR_STATE, "AA window reducer callback failed");
+  return SG_OK;
+}
 
 double& G(sg_aa* a, int i, int j) { return a->gram[(size_t)i * a->memory + j]; }
 
@@ -654,7 +666,7 @@ int qr_pass(sg_aa* a, const T* col, int nq, const double* h, int mode, std::vect
   o->resize(na);
   SG_CK(cudaMemcpyAsync(o->data(), a->out, na * sizeof(double), cudaMemcpyDeviceToHost, a->stream));
   SG_CK(cudaStreamSynchronize(a->stream));
-  return SG_OK;
+  return reduce_sums(a, o->data(), na);
 }
 
 // Thin QR of the current window (oldest column first) by CGS2 appends, the
@@ -765,6 +777,7 @@ int explicit_resid(sg_aa* a, const std::vector<double>& gmm, double& out) {
   double r2 = 0.0;
   SG_CK(cudaMemcpyAsync(&r2, a->out, sizeof(double), cudaMemcpyDeviceToHost, a->stream));
   SG_CK(cudaStreamSynchronize(a->stream));
+  SG_TRY(reduce_sums(a, &r2, 1));
   out = std::sqrt(std::max(r2, 0.0));
   return SG_OK;
 }
@@ -868,6 +881,7 @@ int push_t(sg_aa* a, const void* p, const void* g) {
   std::vector<double> o(na);
   SG_CK(cudaMemcpyAsync(o.data(), a->out, na * sizeof(double), cudaMemcpyDeviceToHost, a->stream));
   SG_CK(cudaStreamSynchronize(a->stream));
+  SG_TRY(reduce_sums(a, o.data(), na));
   a->have_w = false;
   if (first) {
     // memory 0 keeps only the latest entry; otherwise this is fs[0]
@@ -981,6 +995,13 @@ int sg_aa_destroy(sg_aa* a) {
 int sg_aa_set_stream(sg_aa* a, void* s) {
   if (!a) return fail(SG_ERR_ARG, "null window");
   a->stream = reinterpret_cast<cudaStream_t>(s);
+  return SG_OK;
+}
+
+int sg_aa_set_reducer(sg_aa* a, sg_reduce_fn fn, void* ctx) {
+  if (!a) return fail(SG_ERR_ARG, "null window");
+  a->reduce = fn;
+  a->reduce_ctx = ctx;
   return SG_OK;
 }
 

@@ -12,4 +12,12 @@ $NCU -s 4 -c 2 -f -o "$OUT/ncu_fwd_c3" python tools/profile_step.py --config c3 
 $NCU -s 12 -c 2 -f -o "$OUT/ncu_adj_c3" python tools/profile_step.py --config c3 --reps 2 > "$OUT/ncu_adj_c3.log" 2>&1
 $NCU -s 4 -c 2 -f -o "$OUT/ncu_fwd_c5" python tools/profile_step.py --config c5 --recon boundary --shots 8 --nt 400 --reps 2 > "$OUT/ncu_fwd_c5.log" 2>&1
 $NCU -s 12 -c 2 -f -o "$OUT/ncu_adj_c5" python tools/profile_step.py --config c5 --recon boundary --shots 8 --nt 400 --reps 2 > "$OUT/ncu_adj_c5.log" 2>&1
-ls -la "$OUT"/*.ncu-rep
+# summaries on the box (the reports are ~20 MB each with sources; gpurun
+# brings back at most 64 MiB): key metrics, and the hottest source lines
+for r in fwd_c3 adj_c3 fwd_c5 adj_c5; do
+  python tools/ncu_summary.py "$OUT/ncu_$r.ncu-rep" > "$OUT/ncu_$r.txt" 2>&1
+  ncu -i "$OUT/ncu_$r.ncu-rep" --page source --csv --print-source cuda 2>/dev/null \
+      | python tools/ncu_hot_lines.py > "$OUT/ncu_${r}_hot_lines.txt" 2>&1
+  [ "${KEEP_REP:-}" = "$r" ] || rm -f "$OUT/ncu_$r.ncu-rep"
+done
+ls -la "$OUT"
