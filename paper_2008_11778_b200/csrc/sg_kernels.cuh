@@ -101,6 +101,21 @@ constexpr int kHalo = 4;
 #ifndef SG_INNER_LOCK
 #define SG_INNER_LOCK 0
 #endif
+// The fused reverse + adjoint kernel keeps two code paths: interior tiles
+// without damping, every other tile through the generic (edge-tested) path
+// (frame tiles are ~5 % of a C5 plane).  Measured slower (spills: C5 step
+// 120.5 -> 128.9 us, profiles/r02h_ab_c5_rb.log), so off.
+#ifndef SG_INNER_RB
+#define SG_INNER_RB 0
+#endif
+// fp32 adjoint Laplacian with second differences as (u_{-k} + u_{+k}) - 2u
+// (2 adds per tap pair instead of 3).  The adjoint sweep is insensitive to
+// this rounding (fp64 forward + fp32 adjoint: gradient error 1.05e-6 vs
+// 8.2e-7 at C1 iterate 0, 4.2e-6 vs 5.1e-6 at iterate 19, NumPy emulation);
+// the forward keeps the difference form, where it costs 2.5x in accuracy.
+#ifndef SG_ADJ_SUM
+#define SG_ADJ_SUM 1
+#endif
 #ifndef SG_GC
 #if defined(SG_EXPERIMENTAL) && SG_EXPERIMENTAL
 #define SG_GC 0  // the opt-in two-step / resident kernels keep the round-1 arithmetic
@@ -706,7 +721,8 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
       // (odd offsets re-paired from their aligned neighbours)
       // second-difference sums t_k = (u_{-k} - u) + (u_{+k} - u) of the pair,
       // vertical (tz) and horizontal (tx), k = 1..R
-      auto taps = [&](const P* w, const T* s, int q, P* tz, P* tx) {
+      auto taps = [&](const P* w, const T* s, int q, P* tz, P* tx, auto sum_tag) {
+        constexpr bool SUMF = decltype(sum_tag)::value;
         const P uc = w[q + R];
         const T* row = s + (q + R) * SW;
         P xm[R + 1], xp[R + 1];
@@ -724,15 +740,24 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
           xm[4] = m4;
           xp[4] = p4;
         }
+        if constexpr (SUMF) {
+          const P u2 = uc + uc;
 #pragma unroll
-        for (int kk = 1; kk <= R; ++kk) {
-          tz[kk] = (w[q + R - kk] - uc) + (w[q + R + kk] - uc);
-          tx[kk] = (xm[kk] - uc) + (xp[kk] - uc);
+          for (int kk = 1; kk <= R; ++kk) {
+            tz[kk] = (w[q + R - kk] + w[q + R + kk]) - u2;
+            tx[kk] = (xm[kk] + xp[kk]) - u2;
+          }
+        } else {
+#pragma unroll
+          for (int kk = 1; kk <= R; ++kk) {
+            tz[kk] = (w[q + R - kk] - uc) + (w[q + R + kk] - uc);
+            tx[kk] = (xm[kk] - uc) + (xp[kk] - uc);
+          }
         }
       };
-      auto lap2 = [&](const P* w, const T* s, int q) -> P {
+      auto lap2 = [&](const P* w, const T* s, int q, auto sum_tag) -> P {
         P tz[R + 1], tx[R + 1];
-        taps(w, s, q, tz, tx);
+        taps(w, s, q, tz, tx, sum_tag);
         P lz = P::make(T(0), T(0)), lx = P::make(T(0), T(0));
 #pragma unroll
         for (int kk = 1; kk <= R; ++kk) {
@@ -749,10 +774,10 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
       // L u / K
       auto lapf = [&](const P* w, const T* s, int q) -> P {
         if constexpr (!GC) {
-          return lap2(w, s, q);
+          return lap2(w, s, q, std::false_type{});
         } else {
           P tz[R + 1], tx[R + 1];
-          taps(w, s, q, tz, tx);
+          taps(w, s, q, tz, tx, std::false_type{});
           P lz = tz[1], lx = tx[1];
 #pragma unroll
           for (int kk = 2; kk <= R; ++kk) {
@@ -884,7 +909,9 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
         if (!FULL && q >= nq) continue;
         const P ucs = col[q + R];
         const P sv = lds2(sst + q * kBX);
-        P lp = ADJ ? lap2(col, sc, q) : lapf(col, sc, q);
+        // (adjoint: sum-form second differences in fp32, SG_ADJ_SUM)
+        P lp = ADJ ? lap2(col, sc, q, std::bool_constant<SG_ADJ_SUM && sizeof(T) == 4>{})
+                   : lapf(col, sc, q);
         if (!ADJ) {
           if (GSRC) lp = P::fma(ldg2(gin + q * ldx), ldg2(a.gscale + o0 + q * ldx), lp);
           // LOCK: the scattered step, driven by the background's a0_n
@@ -958,8 +985,9 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
       }
       };
       constexpr bool INNER = SG_INNER && !RB && (SG_INNER_LOCK || !LOCK);
-      if (INNER && tile_inner) rows(std::true_type{}, std::false_type{});
-      else if (nq == kNY && vj1) rows(std::true_type{}, std::true_type{});
+      constexpr bool INNER_RB = SG_INNER && SG_INNER_RB && RB;
+      if ((INNER || INNER_RB) && tile_inner) rows(std::true_type{}, std::false_type{});
+      else if (!INNER_RB && nq == kNY && vj1) rows(std::true_type{}, std::true_type{});
       else rows(std::false_type{}, std::true_type{});
     }
     __syncthreads();  // stage (k % NS) is free for shot k + NS

@@ -10,8 +10,9 @@ def main():
     if not rows:
         print("no source page")
         return
-    # the source page repeats a header per kernel; take the first
-    hdr = rows[0]
+    # the page starts with file-name rows; the header is the first row that
+    # names a "Source" column (repeated per kernel: the first is used)
+    hdr = next((r for r in rows if any(c.strip() == "Source" for c in r)), rows[0])
 
     def col(*names):
         for n in names:
@@ -26,7 +27,7 @@ def main():
         print("columns:", hdr)
         return
     data = []
-    for r in rows[1:]:
+    for r in rows:
         if r == hdr or len(r) <= max(si, ws):
             continue
         try:
