@@ -116,6 +116,10 @@ constexpr int kHalo = 4;
 #ifndef SG_ADJ_SUM
 #define SG_ADJ_SUM 1
 #endif
+// (One combined second difference per tap ring when dx == dz -- 22 instead of
+// 26 packed operations, same accuracy -- measured slower: one serial FMA chain
+// instead of two, C3 adjoint step 13.5 vs 12.8 us, profiles/r02j_ab_*_iso.log;
+// the fully expanded c_0 u + sum c_k S_k form is 25x less accurate.)
 #ifndef SG_GC
 #if defined(SG_EXPERIMENTAL) && SG_EXPERIMENTAL
 #define SG_GC 0  // the opt-in two-step / resident kernels keep the round-1 arithmetic
@@ -566,6 +570,21 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
     fence_barrier_init();
   }
   __syncthreads();
+  // shots of the group with a source tap inside this tile: lane k tests shot
+  // k, every warp ballots the same mask
+  unsigned src_mask = 0;
+  if (SRC && a.src_rc != nullptr) {
+    const int lane = tid & 31;
+    bool hit = false;
+    if (lane < nb) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int r = s_src[(lane * 4 + t) * 2], c = s_src[(lane * 4 + t) * 2 + 1];
+        hit |= (r >= i0 && r < i0 + kTH && c >= j0 && c < j0 + kBX);
+      }
+    }
+    src_mask = __ballot_sync(0xffffffffu, hit);
+  }
   auto issue = [&](int k) {
     const int s = k % NS;
     T* st = sbase + s * SM::STAGE;
@@ -675,15 +694,9 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
     const int b = b0 + k;
     if (tid == 0 && k + NS - 1 < nb) issue(k + NS - 1);
 
-    // does this tile hold a source tap of shot b?  (CTA-uniform)
-    bool src_here = false;
-    if (SRC && a.src_rc != nullptr) {
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int r = s_src[(k * 4 + t) * 2], c = s_src[(k * 4 + t) * 2 + 1];
-        src_here |= (r >= i0 && r < i0 + kTH && c >= j0 && c < j0 + kBX);
-      }
-    }
+    // does this tile hold a source tap of shot b?  (CTA-uniform; one bit per
+    // shot of the group, found once in the prologue)
+    const bool src_here = SRC && ((src_mask >> k) & 1u) != 0;
     // receiver injection rows inside this tile?  (CTA-uniform)
     const bool inj_here = ADJ && a.ybar != nullptr && a.inj_row0 < i0 + kTH &&
                           a.inj_row0 + a.inj_nrows > i0;

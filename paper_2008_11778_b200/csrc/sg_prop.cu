@@ -671,7 +671,7 @@ int step_args(sg_handle* h, StepArgs<T>& a, void* F0, void* F1, void* S0, void* 
   };
   for (int k = 1; k < 5; ++k) split(h->cz[1] != 0.0 ? h->cz[k] / h->cz[1] : 0.0, a.rh[k], a.rl[k]);
   split(h->cx[1] / h->cz[1], a.rhoh, a.rhol);
-  a.iso = (a.rhoh == (T)1 && a.rhol == (T)0) ? 1 : 0;
+  a.iso = (a.rhoh == (T)1 && a.rhol == (T)0 && h->cz[1] == h->cx[1]) ? 1 : 0;
   a.cdt2 = (T)(h->d.dt * h->d.dt / h->kfold);
   a.ez = reinterpret_cast<const T*>(h->ez_buf) + kGuard;
   a.ex = reinterpret_cast<const T*>(h->ex_buf) + kGuard;

@@ -18,6 +18,6 @@ for r in fwd_c3 adj_c3 fwd_c5 adj_c5; do
   python tools/ncu_summary.py "$OUT/ncu_$r.ncu-rep" > "$OUT/ncu_$r.txt" 2>&1
   ncu -i "$OUT/ncu_$r.ncu-rep" --page source --csv --print-source cuda 2>/dev/null \
       | python tools/ncu_hot_lines.py > "$OUT/ncu_${r}_hot_lines.txt" 2>&1
-  [ "${KEEP_REP:-}" = "$r" ] || rm -f "$OUT/ncu_$r.ncu-rep"
+  case " ${KEEP_REP:-} " in *" $r "*) ;; *) rm -f "$OUT/ncu_$r.ncu-rep" ;; esac
 done
 ls -la "$OUT"
