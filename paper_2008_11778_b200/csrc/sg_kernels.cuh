@@ -585,8 +585,7 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
     }
     src_mask = __ballot_sync(0xffffffffu, hit);
   }
-  auto issue = [&](int k) {
-    const int s = k % NS;
+  auto issue = [&](int k, int s) {  // shot k of the group into ring stage s (= k % NS)
     T* st = sbase + s * SM::STAGE;
     const int b = b0 + k;
     constexpr uint32_t bytes =
@@ -612,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
   // the L2 round trip of the model loads, then that of the tiles).
   if (tid == 0) {
     pdl_wait();
-    for (int k = 0; k < NS - 1 && k < nb; ++k) issue(k);
+    for (int k = 0; k < NS - 1 && k < nb; ++k) issue(k, k);
   }
 #endif
   // this thread: columns (j, j + 1), rows ib .. ib + kNY - 1; every update is
@@ -687,12 +686,27 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
 #endif
 #if !SG_EARLY_TMA
   if (tid == 0)
-    for (int k = 0; k < NS - 1 && k < nb; ++k) issue(k);
+    for (int k = 0; k < NS - 1 && k < nb; ++k) issue(k, k);
 #endif
 
+  // per-shot output pointers and the ring position advance incrementally
+  // (no per-shot 64-bit multiplies, no k / NS and k % NS)
+  T* __restrict__ fout = a.f[a.cur ^ 1] + (int64_t)b0 * a.plane + o0;
+  T* __restrict__ sout = a.state + (int64_t)b0 * a.plane + o0;
+  T* __restrict__ hout = nullptr;
+  if (!ADJ && HIST) hout = a.hist + ((int64_t)b0 * a.hist_steps + a.hist_slot) * a.hplane + o0;
+  const int64_t hstep = (int64_t)a.hist_steps * a.hplane;
+  T* __restrict__ rout = nullptr;   // RB: u_{n-1}
+  T* __restrict__ rsout = nullptr;  // RB: inc_n
+  if (DUAL) {
+    rout = a.rf[a.rcur ^ 1] + (int64_t)b0 * a.plane + o0;
+    rsout = a.rstate + (int64_t)b0 * a.plane + o0;
+  }
+  int stage = 0;
+  uint32_t phase = 0;
   for (int k = 0; k < nb; ++k) {
     const int b = b0 + k;
-    if (tid == 0 && k + NS - 1 < nb) issue(k + NS - 1);
+    if (tid == 0 && k + NS - 1 < nb) issue(k + NS - 1, stage == 0 ? NS - 1 : stage - 1);
 
     // does this tile hold a source tap of shot b?  (CTA-uniform; one bit per
     // shot of the group, found once in the prologue)
@@ -700,27 +714,16 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
     // receiver injection rows inside this tile?  (CTA-uniform)
     const bool inj_here = ADJ && a.ybar != nullptr && a.inj_row0 < i0 + kTH &&
                           a.inj_row0 + a.inj_nrows > i0;
-    const int64_t sb = (int64_t)b * a.plane;
-    T* __restrict__ fout = a.f[a.cur ^ 1] + sb + o0;
-    T* __restrict__ sout = a.state + sb + o0;
-    T* __restrict__ hout = nullptr;
-    if (!ADJ && HIST) hout = a.hist + ((int64_t)b * a.hist_steps + a.hist_slot) * a.hplane + o0;
     const T* __restrict__ gin = nullptr;
     if (GSRC) gin = a.gsrc + (int64_t)b * a.gsrc_stride + o0;
-    T* __restrict__ rout = nullptr;   // RB: u_{n-1}
-    T* __restrict__ rsout = nullptr;  // RB: inc_n
     const T* __restrict__ bsrc = nullptr;
     T* __restrict__ bdst = nullptr;
-    if (DUAL) {
-      rout = a.rf[a.rcur ^ 1] + sb + o0;
-      rsout = a.rstate + sb + o0;
-    }
     if (RB && a.band_slot >= 0)
       bsrc = a.band + (int64_t)b * a.band_stride + (int64_t)a.band_slot * a.nb;
     if (BSAVE) bdst = a.band + (int64_t)b * a.band_stride + (int64_t)a.band_slot * a.nb;
 
-    mbar_wait(&bar[k % NS], (k / NS) & 1);
-    const T* st = sbase + (k % NS) * SM::STAGE;
+    mbar_wait(&bar[stage], phase);
+    const T* st = sbase + stage * SM::STAGE;
     // this thread's column pair in the halo box, from tile row rb - R
     const T* sc = st + (rb + HO) * SW + kHalo + 2 * threadIdx.x;
     const T* sst = st + SM::HALO + rb * kBX + 2 * threadIdx.x;
@@ -1003,7 +1006,18 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
       else if (!INNER_RB && nq == kNY && vj1) rows(std::true_type{}, std::true_type{});
       else rows(std::false_type{}, std::true_type{});
     }
-    __syncthreads();  // stage (k % NS) is free for shot k + NS
+    __syncthreads();  // this stage is free for shot k + NS
+    fout += a.plane;
+    sout += a.plane;
+    if (!ADJ && HIST) hout += hstep;
+    if (DUAL) {
+      rout += a.plane;
+      rsout += a.plane;
+    }
+    if (++stage == NS) {
+      stage = 0;
+      phase ^= 1u;
+    }
   }
   if (IMG) {
 #pragma unroll
