@@ -813,9 +813,11 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
         }
       };
       // forward acceleration a_n of the pair from its Laplacian (+ point source)
-      auto accel = [&](P lp, int q) -> P {
+      // (src_tag false: a path that never sees a source tile, see the dispatch
+      // below -- the injection code vanishes from it)
+      auto accel = [&](P lp, int q, auto src_tag) -> P {
         P acc = lp * im[q];
-        if (src_here) {
+        if (decltype(src_tag)::value && src_here) {
           const int i = ib + q;
           T a0, a1, m0, m1;
           acc.split(a0, a1);
@@ -876,7 +878,7 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
 #pragma unroll
           for (int q = 0; q < kNY; ++q) {
             if (!FULL && q >= nq) continue;
-            const P acc = accel(lapf(colu, scu, q), q);
+            const P acc = accel(lapf(colu, scu, q), q, std::bool_constant<!FULL>{});
             accs[q] = acc;
             if (HIST) put(hout + q * ldx, acc);
             const P so = inc_next(acc, lds2(sinc + q * kBX), q);
@@ -891,7 +893,7 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
 #pragma unroll
           for (int q = 0; q < kNY; ++q) {
             if (!FULL && q >= nq) continue;
-            const P acc = accel(lapf(colu, scu, q), q);
+            const P acc = accel(lapf(colu, scu, q), q, std::bool_constant<!FULL>{});
             accs[q] = acc;
             P um1;
             if constexpr ((FL & FL_REV3) != 0) {
@@ -933,7 +935,7 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
           // LOCK: the scattered step, driven by the background's a0_n
           // (seisopt/wavesim.py:289-290; no point source)
           if (LOCK) lp = P::fma(accs[q], ldg2(a.gscale + o0 + q * ldx), lp);
-          const P acc = LOCK ? lp * im[q] : accel(lp, q);
+          const P acc = LOCK ? lp * im[q] : accel(lp, q, std::bool_constant<!FULL>{});
           if (BSAVE && tile_band) {
             int bi0, bi1;
             band2(q, bi0, bi1);
@@ -1002,8 +1004,11 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
       };
       constexpr bool INNER = SG_INNER && !RB && (SG_INNER_LOCK || !LOCK);
       constexpr bool INNER_RB = SG_INNER && SG_INNER_RB && RB;
-      if ((INNER || INNER_RB) && tile_inner) rows(std::true_type{}, std::false_type{});
-      else if (!INNER_RB && nq == kNY && vj1) rows(std::true_type{}, std::true_type{});
+      // The tile of a shot's source taps (one in ~176 at C3) takes the generic
+      // path, which alone carries the point-source injection; the two fast
+      // paths are source-free at compile time (bitwise the same updates).
+      if (!src_here && (INNER || INNER_RB) && tile_inner) rows(std::true_type{}, std::false_type{});
+      else if (!src_here && !INNER_RB && nq == kNY && vj1) rows(std::true_type{}, std::true_type{});
       else rows(std::false_type{}, std::true_type{});
     }
     __syncthreads();  // this stage is free for shot k + NS
