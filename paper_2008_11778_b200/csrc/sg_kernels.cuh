@@ -741,34 +741,44 @@ __global__ void __launch_bounds__(kThreads, (step_min_blocks<T, ADJ, FL>()))
         constexpr bool SUMF = decltype(sum_tag)::value;
         const P uc = w[q + R];
         const T* row = s + (q + R) * SW;
-        P xm[R + 1], xp[R + 1];
+        // Horizontal neighbours: even offsets are aligned pairs; the odd
+        // offsets (u[j-1], u[j]) ... straddle two aligned pairs, and building
+        // them as packed operands costs two register moves each, so their
+        // first operation runs on the scalar halves instead (results land in
+        // an aligned register pair; bitwise the packed arithmetic)
         const P m2 = lds2(row - 2), p2 = lds2(row + 2);
-        xm[1] = P::make(m2.hi(), uc.lo());
-        xp[1] = P::make(uc.hi(), p2.lo());
-        if constexpr (R >= 2) {
-          xm[2] = m2;
-          xp[2] = p2;
-        }
+        T ul, uh, m2l, m2h, p2l, p2h;
+        uc.split(ul, uh);
+        m2.split(m2l, m2h);
+        p2.split(p2l, p2h);
+        P m4 = m2, p4 = p2;
+        T m4l = T(0), m4h = T(0), p4l = T(0), p4h = T(0);
         if constexpr (R >= 4) {
-          const P m4 = lds2(row - 4), p4 = lds2(row + 4);
-          xm[3] = P::make(m4.hi(), m2.lo());
-          xp[3] = P::make(p2.hi(), p4.lo());
-          xm[4] = m4;
-          xp[4] = p4;
+          m4 = lds2(row - 4);
+          p4 = lds2(row + 4);
+          m4.split(m4l, m4h);
+          p4.split(p4l, p4h);
         }
         if constexpr (SUMF) {
           const P u2 = uc + uc;
-#pragma unroll
-          for (int kk = 1; kk <= R; ++kk) {
-            tz[kk] = (w[q + R - kk] + w[q + R + kk]) - u2;
-            tx[kk] = (xm[kk] + xp[kk]) - u2;
+          tx[1] = P::make(m2h + uh, ul + p2l) - u2;
+          if constexpr (R >= 2) tx[2] = (m2 + p2) - u2;
+          if constexpr (R >= 4) {
+            tx[3] = P::make(m4h + p2h, m2l + p4l) - u2;
+            tx[4] = (m4 + p4) - u2;
           }
+#pragma unroll
+          for (int kk = 1; kk <= R; ++kk) tz[kk] = (w[q + R - kk] + w[q + R + kk]) - u2;
         } else {
-#pragma unroll
-          for (int kk = 1; kk <= R; ++kk) {
-            tz[kk] = (w[q + R - kk] - uc) + (w[q + R + kk] - uc);
-            tx[kk] = (xm[kk] - uc) + (xp[kk] - uc);
+          const T du = uh - ul;  // (u[j+1] - u[j]) serves both cells of the pair
+          tx[1] = P::make((m2h - ul) + du, (p2l - uh) - du);
+          if constexpr (R >= 2) tx[2] = (m2 - uc) + (p2 - uc);
+          if constexpr (R >= 4) {
+            tx[3] = P::make((m4h - ul) + (p2h - ul), (m2l - uh) + (p4l - uh));
+            tx[4] = (m4 - uc) + (p4 - uc);
           }
+#pragma unroll
+          for (int kk = 1; kk <= R; ++kk) tz[kk] = (w[q + R - kk] - uc) + (w[q + R + kk] - uc);
         }
       };
       auto lap2 = [&](const P* w, const T* s, int q, auto sum_tag) -> P {
