@@ -423,9 +423,12 @@ __device__ __forceinline__ void st2(T* p, V2<T> v) {
 // two stages of {halo'd field tile, state tile[, history tile (adjoint)]}
 // (RB: the fused reverse-forward + adjoint step of boundary-saving
 // reconstruction; a stage then holds {adjoint halo, w tile, u halo, inc tile})
+#ifndef SG_RB_STAGES
+#define SG_RB_STAGES 2  // ring depth of the fp32 dual-field kernels (fused reverse + adjoint, lock-step Born)
+#endif
 template <typename T, bool ADJ, bool RB>
 __host__ __device__ constexpr int step_stages() {
-  return (sizeof(T) != 4 || RB) ? 2 : (ADJ ? SG_ADJ_STAGES : SG_FWD_STAGES);
+  return sizeof(T) != 4 ? 2 : (RB ? SG_RB_STAGES : (ADJ ? SG_ADJ_STAGES : SG_FWD_STAGES));
 }
 
 template <typename T, int R, bool ADJ, bool RB = false>
@@ -482,6 +485,9 @@ __host__ __device__ constexpr int step_min_blocks() {
 #endif
 #ifdef SG_FWD_CTAS
   if (sizeof(T) == 4 && !ADJ && !step_dual<ADJ, FL>()) return SG_FWD_CTAS;
+#endif
+#ifdef SG_RB_CTAS
+  if (sizeof(T) == 4 && ADJ && step_dual<ADJ, FL>()) return SG_RB_CTAS;
 #endif
   return (8 / kTY) * (sizeof(T) != 4 ? (step_dual<ADJ, FL>() ? 1 : 2)
                                      : (step_dual<ADJ, FL>() ? 2 : (ADJ ? SG_ADJ_MINB : SG_FP32_MINB)));
