@@ -6,27 +6,41 @@
 // elements); buffers are [lead row][shot 0 plane][shot 1 plane]...[tail].
 // Columns nxp..ldx-1 stay zero.  Field pointers point at row 0 col 0 of shot 0.
 //
-// One CTA owns a 64 x 32 tile for a GROUP of G shots.  The halo'd field tile
-// (72 x 40) of each shot is brought into shared memory by TMA
-// (cp.async.bulk.tensor.2d, out-of-bounds zero fill == the reference's
-// zero-Dirichlet exterior, seisopt/wavesim.py:216-223), double-buffered so
-// shot k+1 streams in while shot k computes.  Per-cell model data (1/m,
-// sponge factor) stay in registers across the group; each thread owns 8
-// consecutive rows of one column and keeps the vertical stencil window in
-// registers (z-marching inside the tile), so a cell costs ~10 shared loads.
+// One CTA (128 threads) owns a 64 x 16 tile for a GROUP of G shots.  The
+// halo'd field tile (72 x 24) of each shot is brought into shared memory by TMA
+// (cp.async.bulk.tensor.3d, out-of-bounds zero fill == the reference's
+// zero-Dirichlet exterior, seisopt/wavesim.py:216-223) through a ring of 2-3
+// stages tracked by mbarriers, so later shots stream in while shot k computes.
+// Per-cell model data (1/m, sponge factor) stay in registers across the group;
+// each thread owns two adjacent columns x 4 rows, keeps the vertical stencil
+// window of its column pair in registers (z-marching inside the tile) and
+// updates the pair with packed f32x2 arithmetic.
 //
 // Forward (FWD) and adjoint (ADJ) share the kernel shape:
 //   FWD  a_n = inv_m (L u_n [+ g_n s]) [+ amp_n w_k inv_m at the source taps]
 //        inc_{n+1} = d (inc_n + dt^2 a_n),   u_{n+1} = d u_n + inc_{n+1}
 //        (reference: u_{n+1} = d (2 u_n - p_n + dt^2 a_n), p_{n+1} = d u_n,
 //         with inc_n = u_n - p_n -- the increment form keeps fp32 accurate)
-//   ADJ  state V_n = v_n = dt^2 inv_m d lam_{n+1} (seisopt/wavesim.py:331-333)
-//        w_n = d w_{n+1} + L V_n + R^T y_n,   V_{n-1} = d V_n + (dt^2 inv_m d) w_n
+//        fp32 (SG_GC): every global constant of this recursion is kept exact
+//        (weights as ratios to c_1 with hi + lo parts, the z scale folded into
+//        the model plane, dt^2 as hi + lo, d as 1 - e): a constant rounded
+//        once is a coherent phase error that grows with the step count.
+//   ADJ  state V_n = v_n = dt^2 inv_m d lam_{n+1} (seisopt/wavesim.py:331-333),
+//        three-level form (FL_ADJ3, default)
+//          V_{n-1} = coef (L V_n + R^T y_n) + d (2 V_n - d V_{n+1}),
+//          coef = dt^2 d inv_m,
+//        or the V/w increment form
+//          w_n = d w_{n+1} + L V_n + R^T y_n,  V_{n-1} = d V_n + coef w_n;
 //        image -= a_n V_n                       (seisopt/wavesim.py:342-343)
-//        (reference lam_n = L v_n + 2 d lam_{n+1} + d pbar + R^T y with
-//         w_n = lam_n - d lam_{n+1}; algebraically identical, exact transpose)
+//        (reference lam_n = L v_n + 2 d lam_{n+1} - d^2 lam_{n+2} + R^T y_n:
+//         algebraically identical, the exact transpose)
 //   L is applied in difference form sum_k c_k ((u_{+k}-u) + (u_{-k}-u)),
-//   identical to the reference stencil because c_0 = -2 sum_{k>0} c_k.
+//   identical to the reference stencil because c_0 = -2 sum_{k>0} c_k; the
+//   fp32 adjoint, which is insensitive to that rounding, uses
+//   (u_{-k} + u_{+k}) - 2u (SG_ADJ_SUM).
+//   Tiles without a sponge cell skip the damping arithmetic (SG_INNER); the
+//   tile that holds a shot's source taps takes the generic (edge-tested) path,
+//   which alone carries the point-source injection.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
