@@ -123,3 +123,75 @@ def test_c5_grid_gradient_vs_oracle(dtype, recon):
     assert abs(v - c["val"]) <= tol * abs(c["val"])
     assert rel(g.double().cpu().numpy(), c["grad"]) <= tol
     p.close()
+
+
+def test_c5_full_length_fp32_vs_fp64():
+    """BASELINE C5 at its full length (1001 x 3001 grid, nt 12000), the centre
+    shot: the fp32 production path (boundary saving: 12000 fp32 reverse steps)
+    against the fp64 path of the same library on the same inputs -- the fp64
+    path is pinned to the reference at the sizes the CPU oracle can run
+    (test_c5_grid_gradient_vs_oracle, 1e-10).  Observed data from the true
+    model (fp64 synthesis), so the residual is the real one: misfit and
+    gradient within north_star's 1e-4."""
+    from paper_2008_11778_b200 import synthetic, wavesim
+    from paper_2008_11778_b200.model import AcquisitionGeometry
+    case = synthetic.layered_case("c5")
+    g0 = case["geometry"]
+    geom = AcquisitionGeometry((g0.sources[120],), g0.receivers, g0.dt, g0.nt)
+    args = (case["grid"], geom, case["wavelet"], case["config"])
+    p64 = wavesim.Propagator(*args, dtype="float64", recon="checkpoint")
+    p64.set_model(case["true"].m)
+    obs = p64.synthetic().clone()
+    p64.set_model(case["init"].m)
+    v64, g64 = p64.gradient(obs)
+    g64 = g64.cpu().numpy()
+    p64.close()
+    del p64
+    torch.cuda.empty_cache()
+    p32 = wavesim.Propagator(*args, dtype="float32", recon="boundary")
+    p32.set_model(case["init"].m)
+    v32, g32 = p32.gradient(obs.float())
+    assert p32.query()["recon"] == "boundary"
+    p32.close()
+    err = rel(g32.double().cpu().numpy(), g64)
+    print(f"C5 full length, one shot: fp32 boundary vs fp64 gradient {err:.2e}, "
+          f"misfit {abs(v32 - v64) / v64:.2e}")
+    assert abs(v32 - v64) <= F32 * v64
+    assert err <= F32
+
+
+def test_c4_full_length_lsrtm_fp32_vs_fp64():
+    """BASELINE C4 at its full length (201 x 601, nt 6000, 15 Hz), shot 17: Born
+    data and the LSRTM value / gradient of the fp32 production path against
+    the fp64 path of the same library (pinned to the reference over the first
+    1500 steps, test_c4_grid_lsrtm_vs_oracle), background cached and
+    recomputed in lock-step."""
+    from paper_2008_11778_b200 import wavesim
+    case = _one_shot("c4", 17, 6000)
+    args = (case["grid"], case["geometry"], case["wavelet"], case["config"])
+    dm = case["reflectivity"].m_r
+    out = {}
+    for dtype in ("float64", "float32"):
+        for cached in (True, False):
+            p = wavesim.Propagator(*args, dtype=dtype)
+            p.set_model(case["background"].m)
+            if cached:
+                p.born_cache()
+            d = p.born_forward(dm)
+            d_obs = out[("float64", True)][0] if ("float64", True) in out else d
+            v, g = p.lsrtm_gradient(0.5 * dm, d_obs.to(d.dtype))
+            out[(dtype, cached)] = (d.double(), v, g.double().cpu().numpy())
+            p.close()
+            del p
+            torch.cuda.empty_cache()
+    d64, v64, g64 = out[("float64", True)]
+    # fp64: lock-step == cached to round-off
+    assert rel(out[("float64", False)][2], g64) <= F64
+    for cached in (True, False):
+        d32, v32, g32 = out[("float32", cached)]
+        derr = float(torch.linalg.vector_norm(d32 - d64) / torch.linalg.vector_norm(d64))
+        gerr = rel(g32, g64)
+        print(f"C4 full length, cached={cached}: Born data {derr:.2e}, LSRTM value "
+              f"{abs(v32 - v64) / abs(v64):.2e}, gradient {gerr:.2e}")
+        assert derr <= F32 and gerr <= F32
+        assert abs(v32 - v64) <= F32 * abs(v64)
