@@ -202,3 +202,45 @@ def test_nonfinite_guard_warns():
     assert prop.last_nonfinite > 0
     assert not bool(torch.isfinite(grad).all())
     prop.close()
+
+
+def test_aa_window_c2_full_size_fp32_vs_fp64():
+    """BASELINE C2 at its full size (N = 5e7, m = 10, N(0,1) plus a shared
+    smooth rank-3 component): the fp32 production window against the fp64
+    window of the same library (pinned to the reference's AAWindow at small N)
+    on identical inputs, window full and sliding: gamma, residual norm and the
+    recombined iterate."""
+    from paper_2008_11778_b200 import anderson
+    n, m = 50_000_000, 10
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(0)
+    t = torch.linspace(0.0, 1.0, n, device="cuda", dtype=torch.float32)
+    modes = [np.sqrt(2.0) * torch.sin(2.0 * np.pi * (j + 1) * t) for j in range(3)]
+    del t
+    w32 = anderson.AAWindow(n, m, dtype="float32")
+    w64 = anderson.AAWindow(n, m, dtype="float64")
+    worst = (0.0, 0.0, 0.0)
+    for k in range(m + 4):
+        pair = []
+        for _ in range(2):
+            v = torch.randn(n, generator=gen, device="cuda", dtype=torch.float32)
+            c = torch.randn(3, generator=gen, device="cuda", dtype=torch.float32).tolist()
+            for j in range(3):
+                v.add_(modes[j], alpha=c[j])
+            pair.append(v)
+        w32.push(*pair)
+        w64.push(pair[0].double(), pair[1].double())
+        del pair
+        assert w32.m_k == w64.m_k == min(k, m)
+        if not w64.m_k:
+            continue
+        a32, a64 = anderson.aa_weights(w32), anderson.aa_weights(w64)
+        s32 = anderson.aa_step(w32, weights=a32)
+        s64 = anderson.aa_step(w64, weights=a64)
+        ge = float(np.linalg.norm(a32.gamma - a64.gamma) / np.linalg.norm(a64.gamma))
+        re_ = abs(a32.residual_norm - a64.residual_norm) / a64.residual_norm
+        se = float(torch.linalg.vector_norm(s32.double() - s64) / torch.linalg.vector_norm(s64))
+        worst = (max(worst[0], ge), max(worst[1], re_), max(worst[2], se))
+        del s32, s64
+    print(f"C2 full size: gamma {worst[0]:.2e}, residual norm {worst[1]:.2e}, iterate {worst[2]:.2e}")
+    assert worst[0] <= 1e-5 and worst[1] <= 1e-5 and worst[2] <= 1e-6
