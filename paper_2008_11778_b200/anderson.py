@@ -119,12 +119,14 @@ class AAWindow:
         if shard_group is not None and shard_group is not False:
             self._install_reducer(None if shard_group is True else shard_group)
 
-    def _install_reducer(self, group):
+    def _install_reducer(self, group, force=False):
+        """force: install the hook on a one-rank group too (tests of the
+        collective path with one GPU)."""
         torch = _torch()
         import torch.distributed as dist
         if not (dist.is_available() and dist.is_initialized()):
             raise RuntimeError("a sharded AAWindow needs an initialised process group")
-        if dist.get_world_size(group) == 1:
+        if dist.get_world_size(group) == 1 and not force:
             return
         nccl = dist.get_backend(group) == "nccl"
         dev = self.device

@@ -159,6 +159,37 @@ def test_nccl_allreduce_path_one_rank():
     assert abs(j1 - j0) <= 1e-15 * abs(j0)
 
 
+def test_aa_window_nccl_reducer_one_rank():
+    """The N-sharded AA window's reducer hook over NCCL (host sums -> device
+    all-reduce -> host), forced onto a one-rank NCCL group where the
+    all-reduce is the identity: the window must reproduce the reference
+    sequence (aa_window.npz) exactly as the plain window does."""
+    import sys
+    import torch.distributed as dist
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from cases import golden
+    from paper_2008_11778_b200 import anderson
+    g = golden("aa_window")
+    n, memory = int(g["n"]), int(g["memory"])
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}",
+                            rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        win = anderson.AAWindow(n, memory, dtype="float64")
+        win._install_reducer(None, force=True)
+        assert win._reducer is not None
+        plain = anderson.AAWindow(n, memory, dtype="float64")
+        for k in range(len(g["ps"])):
+            win.push(g["ps"][k], g["gs"][k])
+            plain.push(g["ps"][k], g["gs"][k])
+            assert win.m_k == plain.m_k == int(g["m_k"][k])
+            if win.m_k:
+                a, b = anderson.aa_weights(win), anderson.aa_weights(plain)
+                assert np.array_equal(a.gamma, b.gamma) and a.residual_norm == b.residual_norm
+                assert np.allclose(a.gamma, g["gamma"][k][:win.m_k], rtol=1e-10, atol=1e-12)
+    finally:
+        dist.destroy_process_group()
+
+
 def test_redzone_memcheck_small_sweeps():
     """The library's own memcheck (compute-sanitizer is refused on this GPU
     pool): every sweep flavour of the small 60 x 40 case -- fp32/fp64, FULL /
