@@ -16,7 +16,8 @@ offline).
 
 The C3 line also carries ``c5_kernels``: the two boundary-saving step kernels
 of C5 (band-storing forward, fused reverse-forward + adjoint) timed on the
-full 1041 x 3041 padded grid over 8-shot launches -- the HBM-bound case.
+full 1041 x 3041 padded grid over 14-shot launches (the batch a C5 gradient
+runs) -- the HBM-bound case.
 
 metric: Gcell-updates/s = 2 * shots * nt * padded cells per gradient (forward +
 adjoint stencil sweeps; recompute sweeps of checkpoint mode are not counted)
@@ -453,7 +454,7 @@ def shard_report(dist, world, shard, n_shots):
             "shot_ranges": [[int(x[0]), int(x[1])] for x in allt]}
 
 
-def c5_kernel_record(dev, peak, peak_src, reps=400, shots=8, nt=400):
+def c5_kernel_record(dev, peak, peak_src, reps=400, shots=14, nt=400):
     """BASELINE C5's boundary-saving step kernels on the full 1001 x 3001 grid
     (1041 x 3041 padded), `shots`-shot launches as the C5 gradient runs them
     (two concurrent chains): the band-storing forward and the fused
@@ -484,7 +485,8 @@ def c5_kernel_record(dev, peak, peak_src, reps=400, shots=8, nt=400):
     # kmin: the bytes the kernel as designed must move per shot-cell -- forward
     # u, inc in and out (16 B); fused reverse + adjoint with both three-level
     # recurrences: V_n, V_{n+1}, u_n, u_{n+1} in, V_{n-1}, u_{n-1} out (24 B;
-    # the image accumulates per CTA group, the band store is <6 % of cells)
+    # the image read-modify-write adds 8 B per CTA group of up to 8 shots, the
+    # band store is <6 % of cells)
     for name, ms, alg_b, kmin_b in (("forward_band_step", ms_fwd, 4 * es, 4 * es),
                                     ("reverse_adjoint_step", ms_adj, 8 * es + 3 * es, 6 * es)):
         alg = shots * C * alg_b
@@ -527,11 +529,12 @@ def run_ours(args):
     obs_full = torch.zeros((S, nt, geom.n_receivers), dtype=obs_local.dtype, device=dev)
     obs_full[s0:s0 + cnt] = obs_local
     del obs_local
-    # the sweep buffers may take 80 % of what is free once the observed data
-    # are resident (C5: boundary-saving batches of ~12 shots)
+    # the sweep buffers may take 80 % of what is free with the observed data
+    # resident (C5: boundary-saving batches of 13 shots)
     budget = 0.0
     if args.config == "c5":
-        budget = 0.8 * (torch.cuda.mem_get_info(dev)[0] - obs_full.numel() * obs_full.element_size())
+        torch.cuda.empty_cache()  # the synthesis temporaries go back to the driver first
+        budget = 0.8 * torch.cuda.mem_get_info(dev)[0]
     obj = gradients.FwiObjective(grid, obs_full, wav, geom, cfg, dtype=case["dtype"],
                                  device=dev, shard=shard, mem_budget_bytes=budget)
     del obs_full

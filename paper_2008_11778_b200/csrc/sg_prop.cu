@@ -551,7 +551,12 @@ int ensure_batch(sg_handle* h) {
 // ~20 B per shot-cell); the persistent grid holds `slots` CTAs, so the
 // busiest CTA processes ceil(items / slots) * G shots.  Minimise that
 // critical path times the amortisation overhead.
-int group_for(const sg_handle* h, int count, int per_sm = 0) {
+// `amort`: per-CTA overhead in shot-equivalents (prologue, model loads, image
+// read-modify-write).  0.6 for the one-field kernels; 1.5 for the fused
+// reverse + adjoint kernel, whose step time per shot keeps falling with G on
+// the HBM-bound C5 grid (14.5 / 13.9 / 13.5 / 13.3 / 13.1 us for G = 4..8,
+// profiles/r02ag_c5_batch_group.log); its ties go to the larger group.
+int group_for(const sg_handle* h, int count, int per_sm = 0, double amort = 0.6) {
   if (h->d.group > 0) return std::max(1, std::min({h->d.group, count, 8}));
   static int env = -1;
   if (env < 0) {
@@ -565,8 +570,8 @@ int group_for(const sg_handle* h, int count, int per_sm = 0) {
   for (int G = 1; G <= std::min(8, count); ++G) {
     const int64_t items = (int64_t)h->ntiles * ((count + G - 1) / G);
     const double rounds = (double)((items + slots - 1) / slots);
-    const double cost = rounds * G * (1.0 + 0.6 / G);
-    if (cost < best_cost - 1e-9) {
+    const double cost = rounds * G * (1.0 + amort / G);
+    if (amort > 1.0 ? cost <= best_cost + 1e-9 : cost < best_cost - 1e-9) {
       best_cost = cost;
       best = G;
     }
@@ -706,7 +711,7 @@ int launch_step_f(const sg_handle* h, cudaStream_t s, const StepArgs<T>& a0) {
     attr_devs.fetch_or(bit);
   }
   StepArgs<T> a = a0;
-  a.G = group_for(h, a.count, per_sm);
+  a.G = group_for(h, a.count, per_sm, (ADJ && step_dual<ADJ, FL>()) ? 1.5 : 0.6);
   // one-step fp32 adjoint: at most SG_ADJ_GMAX shots per CTA group (C3: 4
   // instead of the cost model's 5 -- adjoint step 14.1 -> 13.3 us,
   // profiles/r01e_ab_group2.log)

@@ -17,8 +17,8 @@ $NCU -k regex:k_step --launch-skip 3000 --launch-count 400 \
     python tools/one_gradient.py --config c3 > "$OUT/traffic_c3_fwd.csv" 2> "$OUT/traffic_c3_fwd.err"
 $NCU -k regex:k_step --launch-skip 11000 --launch-count 400 \
     python tools/one_gradient.py --config c3 > "$OUT/traffic_c3_adj.csv" 2> "$OUT/traffic_c3_adj.err"
-# C5 BOUNDARY: 8-shot steps (band-storing forward, fused reverse + adjoint);
+# C5 BOUNDARY: 14-shot steps (the batch a full C5 gradient runs: two 7-shot chains) (band-storing forward, fused reverse + adjoint);
 # the band store walks a new slot per launch, the fields are far larger than L2
 $NCU -k regex:k_step --launch-count 400 \
-    python tools/profile_step.py --config c5 --recon boundary --shots 8 --nt 400 --reps 40 \
+    python tools/profile_step.py --config c5 --recon boundary --shots 14 --nt 400 --reps 40 \
     > "$OUT/traffic_c5.csv" 2> "$OUT/traffic_c5.err"
