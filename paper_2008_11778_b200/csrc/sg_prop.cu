@@ -1819,12 +1819,26 @@ int copy_gathers_in(sg_handle* h, const void* src, int cnt) {
   return SG_OK;
 }
 
+// Shots of the next batch when `remaining` are left: the fewest batches the
+// buffers allow, balanced (sizes differ by at most one), so a survey that is
+// not a multiple of the batch never ends in a sliver batch at the per-step
+// latency floor (C5: 240 shots at B = 14 ran 17 x 14 + 2; now 6 x 14 + 12 x 13)
+int next_batch(const sg_handle* h, int remaining) {
+  static const bool balance = [] {
+    const char* e = getenv("SG_BALANCE");
+    return !(e && atoi(e) == 0);
+  }();
+  if (!balance) return std::min(h->B, remaining);
+  const int nb = (remaining + h->B - 1) / h->B;
+  return (remaining + nb - 1) / nb;
+}
+
 template <typename T>
 int fwi_synthetic_t(sg_handle* h, int shot0, int count, void* out) {
   SG_TRY(ensure_batch(h));
   const size_t per = (size_t)h->d.nt * h->d.n_rec * h->esz;
-  for (int b0 = shot0; b0 < shot0 + count; b0 += h->B) {
-    const int cnt = std::min(h->B, shot0 + count - b0);
+  for (int b0 = shot0, cnt = 0; b0 < shot0 + count; b0 += cnt) {
+    cnt = next_batch(h, shot0 + count - b0);
     SG_TRY(do_forward_batch<T>(h, b0, cnt, false));
     SG_TRY(copy_gathers_out<T>(h, (char*)out + (size_t)(b0 - shot0) * per, cnt));
   }
@@ -1837,8 +1851,8 @@ int fwi_misfit_t(sg_handle* h, int shot0, int count, const void* obs, double* mi
   SG_TRY(ensure_batch(h));
   SG_CK(cudaMemsetAsync(h->scal, 0, sizeof(double), h->stream));
   const size_t per = (size_t)h->d.nt * h->d.n_rec * h->esz;
-  for (int b0 = shot0; b0 < shot0 + count; b0 += h->B) {
-    const int cnt = std::min(h->B, shot0 + count - b0);
+  for (int b0 = shot0, cnt = 0; b0 < shot0 + count; b0 += cnt) {
+    cnt = next_batch(h, shot0 + count - b0);
     SG_TRY(do_forward_batch<T>(h, b0, cnt, false));
     SG_TRY(residual<T>(h, cnt, reinterpret_cast<const T*>((const char*)obs + (b0 - shot0) * per),
                        2));
@@ -1858,8 +1872,8 @@ int fwi_gradient_t(sg_handle* h, int shot0, int count, const void* obs, double* 
   // phase events per batch (sg_phase_times; printed with SG_PHASE_TIMING=1)
   static const bool timing = getenv("SG_PHASE_TIMING") != nullptr;
   h->ph_batches = 0;
-  for (int b0 = shot0; b0 < shot0 + count; b0 += h->B) {
-    const int cnt = std::min(h->B, shot0 + count - b0);
+  for (int b0 = shot0, cnt = 0; b0 < shot0 + count; b0 += cnt) {
+    cnt = next_batch(h, shot0 + count - b0);
     while ((int)h->ph_ev.size() < 5 * (h->ph_batches + 1)) {
       cudaEvent_t e;
       SG_CK(cudaEventCreate(&e));
@@ -1952,8 +1966,8 @@ int born_cache_t(sg_handle* h, int shot0, int count) {
   h->born_b0 = shot0;
   h->born_count = count;
   const int nt = h->d.nt;
-  for (int b0 = shot0; b0 < shot0 + count; b0 += h->B) {
-    const int cnt = std::min(h->B, shot0 + count - b0);
+  for (int b0 = shot0, cnt = 0; b0 < shot0 + count; b0 += cnt) {
+    cnt = next_batch(h, shot0 + count - b0);
     SG_TRY(load_batch_sources(h, b0, cnt));
     SG_TRY(zero_fields(h, true, false, cnt));
     void* base = (char*)h->born_hist + (size_t)(b0 - shot0) * per;
